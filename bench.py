@@ -1,0 +1,312 @@
+"""Benchmark: voxel stress + AD-tangent evaluations per second (fp64) on B200.
+
+Workload (BASELINE.json configs[1]): 2^20 independent elasto-viscoplastic
+(Michel-Suquet, Table-1) material points per GPU, random strain increments
+(SURVEY.md §8d generator), automatic strategy, implicit Euler, stress +
+second-order AD consistent tangent.  One step = one material evaluation of
+the whole batch.  Multi-GPU: one process per GPU, each rank evaluates its own
+2^20 points (weak scaling, no data-path collective -- the material points are
+independent); the step time is the max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+``--impl reference`` times the reference algorithm's CPU implementation
+(the C restatement in oracle/, all host threads) on a bounded sample of the
+same workload.
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "voxel stress+tangent evals/sec (fp64)"
+UNIT = "evals/s"
+B_DEFAULT = 1 << 20
+
+
+def flops_per_eval(iters, tangent=True):
+    """Algorithmic fp64 flops of one evaluation: 1072 per Newton
+    iteration + 2273 for the tangent post-process, stress and tangent
+    (+38 without tangent)."""
+    return 1072.0 * iters + (2273.0 if tangent else 38.0)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_rate(B, threads, seed=0):
+    """evals/s of the C oracle (reference algorithm) on a B-point sample."""
+    from oracle import material as OM
+    from paper_2006_04391_b200.workloads import config2_batch
+
+    en, an, ep, dt = config2_batch(B, seed=seed)
+    t0 = time.perf_counter()
+    OM.evaluate(OM.ALUMINUM, en, an, ep, dt, True, threads=threads)
+    return B / (time.perf_counter() - t0)
+
+
+def cpu_baseline(target_s=12.0):
+    threads = os.cpu_count() or 1
+    probe = oracle_rate(max(256, 64 * threads), threads, seed=7)
+    B = int(min(1 << 17, max(1024, probe * target_s)))
+    rate = oracle_rate(B, threads, seed=0)
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{B} config-2 points (first {B} of the seeded generator, seed 0), "
+                      f"C restatement of gsmkit automatic implicit-Euler + tangent, {threads} threads, {cpu_model()}"}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": smax, "reasons": sorted(reasons)}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def run_reference(args, rank):
+    """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    probe = oracle_rate(max(256, 32 * threads), threads, seed=7)
+    B = int(min(1 << 16, max(512, probe * 2.0)))  # ~2 s of CPU work per step
+    for _ in range(args.warmup):
+        oracle_rate(B, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle_rate(B, threads)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = B / (ms * 1e-3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config 2 sample: {B} of 2^20 EVP material points, stress + AD tangent",
+                   "law": "MichelSuquet(ALUMINUM_MATRIX)", "strategy": "automatic", "integrator": "implicit-euler"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{B} points per step, C restatement of gsmkit (oracle/material_oracle.c), "
+                                   f"{threads} threads, {cpu_model()}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=B_DEFAULT)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+
+    from paper_2006_04391_b200 import _lib, gsm
+    from paper_2006_04391_b200.evaluator import StrategyConfig
+    from paper_2006_04391_b200.workloads import config2_batch
+
+    lib = _lib.load()
+    _lib.check(lib.am_set_device(local))
+    law = gsm.MichelSuquet()
+    cfg = StrategyConfig(strategy="automatic", integrator="implicit-euler")
+    s_law, s_cfg = _lib.make_law(law), _lib.make_cfg(cfg)
+    B = args.batch
+
+    en, an, ep, dt = config2_batch(B, seed=rank)
+    soa = lambda x: torch.from_numpy(np.ascontiguousarray(x.T)).to(dev)  # noqa: E731
+    d_en, d_an, d_ep = soa(en), soa(an), soa(ep)
+    d_dt = torch.from_numpy(dt).to(dev)
+    d_sig = torch.empty((6, B), dtype=torch.float64, device=dev)
+    d_a = torch.empty((7, B), dtype=torch.float64, device=dev)
+    d_C = torch.empty((36, B), dtype=torch.float64, device=dev)
+    d_it = torch.empty(B, dtype=torch.int32, device=dev)
+    d_fl = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
+    def step():
+        rc = lib.am_eval_batch(s_law, s_cfg, B, d_en.data_ptr(), d_an.data_ptr(), d_ep.data_ptr(), d_dt.data_ptr(),
+                               0.0, 1, d_sig.data_ptr(), d_a.data_ptr(), d_C.data_ptr(), d_it.data_ptr(), None,
+                               d_fl.data_ptr(), sp)
+        if rc:
+            _lib.check(rc)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if int(d_fl.item()) != 0:
+        raise RuntimeError(f"material kernel reported status flags {int(d_fl.item())}")
+
+    # ---- device-resident throughput (inputs in HBM; 552 MiB of I/O per step > 126 MB L2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * B / (ms_max * 1e-3)
+
+    iters = d_it.cpu().numpy()
+    fl = float(np.sum(flops_per_eval(iters.astype(np.float64))))
+    achieved = fl / (ms * 1e-3) / 1e12
+    peak = ctypes.c_double(0.0)
+    _lib.check(lib.am_probe_fp64_tflops(5, ctypes.byref(peak)))
+
+    # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    pin = lambda shape, dtype=torch.float64: torch.empty(shape, dtype=dtype, pin_memory=True).numpy()  # noqa: E731
+    h_en, h_an, h_ep, h_dt = pin((B, 6)), pin((B, 7)), pin((B, 6)), pin((B,))
+    h_en[:], h_an[:], h_ep[:], h_dt[:] = en, an, ep, dt
+    h_sig, h_a, h_C, h_it = pin((B, 6)), pin((B, 7)), pin((B, 6, 6)), pin((B,), torch.int32)
+
+    def e2e_step():
+        rc = lib.am_eval_batch_host(s_law, s_cfg, B, _lib.ptr(h_en), _lib.ptr(h_an), _lib.ptr(h_ep), _lib.ptr(h_dt),
+                                    1, _lib.ptr(h_sig), _lib.ptr(h_a), _lib.ptr(h_C), _lib.ptr(h_it, _lib._i32p), None)
+        _lib.check(rc)
+
+    for _ in range(2):
+        e2e_step()
+    e2e_steps = max(3, min(args.steps, 10))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world * B / float(e2e_t.item())
+    assert np.array_equal(h_it, iters), "e2e path disagrees with the device path"
+    h2d = B * (6 + 7 + 6 + 1) * 8
+    d2h = B * (6 + 7 + 36) * 8 + B * 4
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config 2: {B} EVP material points per GPU, stress + second-order AD tangent",
+                   "law": "MichelSuquet(ALUMINUM_MATRIX)", "strategy": "automatic", "integrator": "implicit-euler",
+                   "batch_per_gpu": B, "parallelism": f"dp{world} (independent points, no collective)",
+                   "l2": "inputs+outputs 552 MiB per step > 126 MB L2 (no flush needed)",
+                   "mean_newton_iters": float(iters.mean())},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+                     "frac": achieved / peak.value if peak.value else None, "traffic": None,
+                     "peak_source": "measured: am_probe_fp64_tflops DFMA microbenchmark on this GPU "
+                                    "(MEASURED_PEAKS.json has no fp64 entry)",
+                     "work_per_launch": f"{fl:.4g} algorithmic fp64 flops (SURVEY §8d: 1072*N_it + 2273 per eval)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "am_eval_batch_host (C ABI), pinned host AoS buffers, 2-stream chunked H2D|kernel|D2H"},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

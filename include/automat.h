@@ -1,0 +1,141 @@
+/*
+ * automat.h -- C ABI of the B200 AutoMat library (libautomat.so).
+ *
+ * Plain C types only: pointers, sizes, POD structs.  This is the boundary
+ * the reference's Python API sits on (the ctypes shim in
+ * paper_2006_04391_b200/_lib.py binds exactly these symbols).  Every entry
+ * point names the reference routine it replaces.
+ *
+ * Layouts
+ *   SoA ("component-major"): element (c, b) of a batch of B items with k
+ *   components lives at p[c * B + b].  Device entry points take SoA device
+ *   pointers; *_host entry points take the reference's AoS host arrays
+ *   ((B, 6), (B, m), (B, 6, 6) row-major, exactly what
+ *   gsmkit.evaluator.evaluate_arrays receives and returns).
+ *   Fields of the basic-scheme solver are component-first (6, Nx, Ny, Nz)
+ *   like gsmkit.homogenize (homogenize.py:12-13).
+ *
+ * Errors: every function returns an am_status; am_last_error() gives a
+ * thread-local message for the last failure on the calling thread.
+ */
+#ifndef AUTOMAT_H
+#define AUTOMAT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- codes */
+typedef enum am_status {
+    AM_OK = 0,
+    AM_ERR_CONFIG = 1,            /* evaluator.ConfigError (evaluator.py:31) */
+    AM_ERR_NEWTON = 2,            /* odeint.NewtonDivergenceError (odeint.py:34, 415-416) */
+    AM_ERR_SINGULAR = 3,          /* linalg.SingularMatrixError (linalg.py:20, 103-104) */
+    AM_ERR_NOT_CONVERGED = 4,     /* homogenize.SolverError (homogenize.py:29-34, 466-471) */
+    AM_ERR_CUDA = 5,
+    AM_ERR_NCCL = 6,
+    AM_ERR_ARG = 7,               /* ValueError on bad arguments */
+    AM_ERR_NONFINITE = 8          /* reference_update: non-finite tangent (homogenize.py:316-317) */
+} am_status;
+
+/* per-voxel status bits written by the material kernel */
+#define AM_VOXEL_NEWTON_FAILED 1u
+#define AM_VOXEL_SINGULAR 2u
+#define AM_VOXEL_NONFINITE 4u
+
+/* ---------------------------------------------------------------- laws
+ * A law is its two potentials; the potentials live on the device.
+ * kind: AM_LAW_LINEAR_ELASTIC -> gsm.LinearElastic(E, nu)      (gsm.py:100-153)
+ *       AM_LAW_MICHEL_SUQUET  -> gsm.MichelSuquet(params)      (gsm.py:210-256)
+ */
+enum { AM_LAW_LINEAR_ELASTIC = 0, AM_LAW_MICHEL_SUQUET = 1 };
+
+typedef struct am_law {
+    int32_t kind;
+    int32_t reserved;
+    double E, nu;                              /* both laws */
+    double sigma_Y, H, eps0_dot, sigma_d, n;   /* MichelSuquetParams (gsm.py:156-174) */
+} am_law;
+
+/* ---------------------------------------------------------------- config
+ * StrategyConfig (evaluator.py:35-74).  Order of the enums follows
+ * STRATEGIES / INTEGRATORS / ERROR_MEASURES (evaluator.py:26-28).  This
+ * build implements strategy=automatic x integrator=implicit-euler; other
+ * combinations return AM_ERR_CONFIG.
+ */
+enum { AM_STRATEGY_CONVENTIONAL = 0, AM_STRATEGY_AUTOMATIC = 1, AM_STRATEGY_SEMI_AUTOMATIC = 2 };
+enum { AM_INTEGRATOR_IMPLICIT_EULER = 0, AM_INTEGRATOR_ODE12 = 1, AM_INTEGRATOR_ODE23 = 2, AM_INTEGRATOR_ODE23S = 3 };
+enum { AM_NEWTON_INTERNAL = 0, AM_NEWTON_STRESS = 1 };
+
+typedef struct am_cfg {
+    int32_t strategy;
+    int32_t integrator;
+    int32_t newton_mode;     /* resolved_newton_mode (evaluator.py:69-71) */
+    int32_t max_newton;      /* 50 (odeint.py:371) */
+    double newton_tol;       /* 1e-10 (odeint.py:404) */
+} am_cfg;
+
+/* ---------------------------------------------------------------- library */
+const char *am_last_error(void);
+const char *am_version(void);
+int am_device_count(int *count);
+int am_set_device(int device);
+
+/* ---------------------------------------------------------------- material points
+ * am_eval_batch -- replaces gsmkit.evaluator.evaluate_arrays
+ * (evaluator.py:206-248) for the automatic implicit-Euler route.
+ * Device pointers, SoA, asynchronous on `stream` (cudaStream_t or NULL).
+ *   eps_n, eps_np1: 6*B      a_n, a_out: m*B (m = 7 Michel-Suquet, 0 elastic)
+ *   dt: B values, or NULL to use dt_scalar for every item
+ *   sigma: 6*B   C: 36*B (C[(i*6+j)*B + b] = dsigma_i/deps_j) or NULL
+ *   newton_iters (int32, B) / status (uint8, B) / flags (one uint32 that
+ *   receives the OR of all status bits): each optional (NULL).
+ * Returns AM_OK once the work is enqueued; per-voxel failures are reported
+ * through status / flags (NewtonDivergenceError / SingularMatrixError are
+ * raised from them by the caller, see am_eval_batch_host).
+ */
+int am_eval_batch(const am_law *law, const am_cfg *cfg, int64_t B,
+                  const double *eps_n, const double *a_n, const double *eps_np1,
+                  const double *dt, double dt_scalar, int want_tangent,
+                  double *sigma, double *a_out, double *C,
+                  int32_t *newton_iters, uint8_t *status, uint32_t *flags, void *stream);
+
+/*
+ * am_eval_batch_host -- same as evaluate_arrays with the reference's host
+ * AoS arrays: eps_n/eps_np1 (B,6), a_n/a_out (B,m), dt (B), sigma (B,6),
+ * C (B,6,6) or NULL.  Pinned or pageable memory.  Synchronous.  The batch is
+ * pipelined through the GPU in chunks over two streams (H2D | kernel | D2H).
+ * Returns AM_ERR_NEWTON if any voxel's Newton failed (odeint.py:415-416),
+ * else AM_ERR_SINGULAR if any tangent LU was singular (odeint.py:424), else
+ * AM_OK.  Outputs are written for every voxel in all cases.
+ */
+int am_eval_batch_host(const am_law *law, const am_cfg *cfg, int64_t B,
+                       const double *eps_n, const double *a_n, const double *eps_np1,
+                       const double *dt, int want_tangent,
+                       double *sigma, double *a_out, double *C,
+                       int32_t *newton_iters, uint8_t *status);
+
+/*
+ * am_constitutive_host -- module-level constitutive operations at B points
+ * (gsm.stress / generalized_stress / evolution_rhs / rhs_jacobian /
+ * rhs_strain_jacobian, gsm.py:574-602), evaluated by the same device AD
+ * routines as the material kernel.  AoS host arrays: eps (B,6), a (B,m);
+ * outputs sigma (B,6), A (B,m), f (B,m), dfda (B,m,m), dfde (B,m,6); any
+ * output may be NULL.
+ */
+int am_constitutive_host(const am_law *law, int64_t B, const double *eps, const double *a,
+                         double *sigma, double *A, double *f, double *dfda, double *dfde);
+
+/* ---------------------------------------------------------------- diagnostics
+ * am_probe_fp64_tflops -- sustained fp64 FMA throughput of the current
+ * device (the roofline denominator of the material kernel; no reference
+ * counterpart).
+ */
+int am_probe_fp64_tflops(int reps, double *tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUTOMAT_H */

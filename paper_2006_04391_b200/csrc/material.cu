@@ -1,0 +1,356 @@
+// material.cu -- K1: the one-thread-per-voxel fp64 material kernel and its
+// C-ABI entry points (am_eval_batch, am_eval_batch_host,
+// am_constitutive_host).
+//
+// Replaces gsmkit.evaluator.evaluate_arrays (evaluator.py:206-248) for
+// StrategyConfig(strategy="automatic", integrator="implicit-euler"): each
+// thread runs material.cuh's eval_voxel -- reverse AD of the two potentials
+// over forward duals, the implicit-Euler Newton, the tangent post-process,
+// clamp, stress and consistent tangent -- with all intermediates in
+// registers.  Inputs and outputs are read/written through (component
+// stride, item stride) pairs so the same kernel serves SoA device fields
+// (coalesced: consecutive threads touch consecutive doubles) and the
+// reference's AoS host layout on the host-pointer path.
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "material.cuh"
+
+namespace am {
+
+struct Layout {
+    int64_t cs, es;  // element (c, b) at p[c * cs + b * es]
+};
+
+struct KArgs {
+    int64_t B;
+    const int64_t* gidx;  // optional gather/scatter index for eps_n / eps_np1 / sigma
+    const double* eps_n;
+    const double* a_n;
+    const double* eps_np1;
+    const double* dt;
+    double dt_scalar;
+    Layout le, la, lc;
+    double* sigma;
+    double* a_out;
+    double* C;
+    int32_t* iters;
+    uint8_t* status;
+    uint32_t* flags;
+    NewtonCfg ncfg;
+};
+
+template <class Law>
+__global__ void __launch_bounds__(128) k_material(Law L, KArgs k) {
+    constexpr int m = Law::m;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = k.gidx ? k.gidx[b] : b;
+        const int64_t eo = g * k.le.es, ao = b * k.la.es;
+        double en[6], e1[6], an[m > 0 ? m : 1], ao_[m > 0 ? m : 1], sig[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            en[c] = __ldg(k.eps_n + c * k.le.cs + eo);
+            e1[c] = __ldg(k.eps_np1 + c * k.le.cs + eo);
+        }
+#pragma unroll
+        for (int c = 0; c < m; ++c) an[c] = __ldg(k.a_n + c * k.la.cs + ao);
+        const double dt = k.dt ? __ldg(k.dt + b) : k.dt_scalar;
+        int it = 0;
+        int st;
+        if (k.C) {
+            double C[6][6];
+            st = eval_voxel(L, k.ncfg, en, an, e1, dt, sig, ao_, C, it);
+            const int64_t co = b * k.lc.es;
+            bool fin = true;
+#pragma unroll
+            for (int i = 0; i < 6; ++i)
+#pragma unroll
+                for (int j = 0; j < 6; ++j) {
+                    k.C[(i * 6 + j) * k.lc.cs + co] = C[i][j];
+                    fin = fin && (C[i][j] - C[i][j] == 0.0);
+                }
+            if (!fin) st |= ST_NONFINITE;
+        } else {
+            st = eval_voxel(L, k.ncfg, en, an, e1, dt, sig, ao_, (double(*)[6]) nullptr, it);
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) k.sigma[c * k.le.cs + eo] = sig[c];
+#pragma unroll
+        for (int c = 0; c < m; ++c) k.a_out[c * k.la.cs + ao] = ao_[c];
+        if (k.iters) k.iters[b] = it;
+        if (k.status) k.status[b] = (uint8_t)st;
+        if (st && k.flags) atomicOr(k.flags, (uint32_t)st);
+    }
+}
+
+// gsm.py:574-602 at B points (AoS); used by the module-level API and the AD
+// unit tests.  eps dirs and a dirs are separate sweeps, like rhs_dual /
+// rhs_and_jac.
+template <class Law>
+__global__ void k_constitutive(Law L, int64_t B, const double* eps, const double* a, double* sigma, double* A,
+                               double* f, double* dfda, double* dfde) {
+    constexpr int m = Law::m;
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double e[6], s[6], av[m > 0 ? m : 1];
+    for (int c = 0; c < 6; ++c) e[c] = eps[6 * b + c];
+    for (int c = 0; c < m; ++c) av[c] = a[m * b + c];
+    stress_plain(L, e, av, s);
+    if (sigma)
+        for (int c = 0; c < 6; ++c) sigma[6 * b + c] = s[c];
+    if constexpr (m > 0) {
+        if (A) {
+            auto Av = gen_stress_sweep(L, plain_tup<6>(e, seq<6>{}), plain_tup<m>(av, seq<m>{}));
+            sfor<m>([&](auto I) { A[m * b + decltype(I)::value] = get<decltype(I)::value>(Av).v; });
+        }
+        double fv[m], J[m][m], Je[m][6];
+        rhs_jac_a(L, e, av, fv, J);
+        rhs_jac_eps(L, e, 1.0, av, Je);
+        for (int i = 0; i < m; ++i) {
+            if (f) f[m * b + i] = fv[i];
+            for (int k = 0; k < m; ++k)
+                if (dfda) dfda[(m * b + i) * m + k] = J[i][k];
+            for (int k = 0; k < 6; ++k)
+                if (dfde) dfde[(m * b + i) * 6 + k] = Je[i][k];
+        }
+    }
+}
+
+static int check_law(const am_law* law) {
+    if (!law) return fail(AM_ERR_ARG, "law is NULL");
+    if (law->kind != AM_LAW_LINEAR_ELASTIC && law->kind != AM_LAW_MICHEL_SUQUET)
+        return fail(AM_ERR_CONFIG, "unknown law kind %d (only LinearElastic and MichelSuquet have device potentials)",
+                    law->kind);
+    return AM_OK;
+}
+
+static int check_cfg(const am_cfg* cfg) {
+    if (!cfg) return fail(AM_ERR_ARG, "cfg is NULL");
+    if (cfg->strategy != AM_STRATEGY_AUTOMATIC || cfg->integrator != AM_INTEGRATOR_IMPLICIT_EULER)
+        return fail(AM_ERR_CONFIG,
+                    "only strategy='automatic' with integrator='implicit-euler' is implemented on the device "
+                    "(got strategy %d, integrator %d)",
+                    cfg->strategy, cfg->integrator);
+    if (cfg->newton_mode != AM_NEWTON_INTERNAL && cfg->newton_mode != AM_NEWTON_STRESS)
+        return fail(AM_ERR_CONFIG, "unknown newton mode %d", cfg->newton_mode);
+    if (cfg->max_newton <= 0) return fail(AM_ERR_ARG, "max_newton must be positive");
+    return AM_OK;
+}
+
+static NewtonCfg newton_cfg(const am_cfg* cfg) { return NewtonCfg{cfg->newton_mode, cfg->max_newton, cfg->newton_tol}; }
+
+static int launch(const am_law* law, const KArgs& k, cudaStream_t s) {
+    if (k.B == 0) return AM_OK;
+    const int threads = 128;
+    int64_t blocks = (k.B + threads - 1) / threads;
+    if (blocks > (int64_t)kSMs * 1024) blocks = (int64_t)kSMs * 1024;
+    if (law->kind == AM_LAW_MICHEL_SUQUET) {
+        auto L = MichelSuquetLaw::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot, law->sigma_d, law->n);
+        k_material<<<(unsigned)blocks, threads, 0, s>>>(L, k);
+    } else {
+        auto L = LinearElasticLaw::make(law->E, law->nu);
+        k_material<<<(unsigned)blocks, threads, 0, s>>>(L, k);
+    }
+    AM_CUDA(cudaGetLastError());
+    return AM_OK;
+}
+
+int law_m(const am_law* law) { return law->kind == AM_LAW_MICHEL_SUQUET ? 7 : 0; }
+
+// internal entry used by the basic-scheme solver: gathers eps fields through
+// gidx, per-material state arrays are SoA with stride Bm.
+int eval_gather(const am_law* law, const am_cfg* cfg, int64_t B, const int64_t* gidx, int64_t N,
+                const double* eps_n, const double* a_n, const double* eps_np1, double dt, int want_tangent,
+                double* sigma, double* a_out, double* C, int32_t* iters, uint8_t* status, uint32_t* flags,
+                cudaStream_t s) {
+    KArgs k{};
+    k.B = B; k.gidx = gidx;
+    k.eps_n = eps_n; k.a_n = a_n; k.eps_np1 = eps_np1; k.dt = nullptr; k.dt_scalar = dt;
+    k.le = {N, 1}; k.la = {B, 1}; k.lc = {B, 1};
+    k.sigma = sigma; k.a_out = a_out; k.C = want_tangent ? C : nullptr;
+    k.iters = iters; k.status = status; k.flags = flags;
+    k.ncfg = newton_cfg(cfg);
+    return launch(law, k, s);
+}
+
+}  // namespace am
+
+using namespace am;
+
+extern "C" int am_eval_batch(const am_law* law, const am_cfg* cfg, int64_t B, const double* eps_n,
+                             const double* a_n, const double* eps_np1, const double* dt, double dt_scalar,
+                             int want_tangent, double* sigma, double* a_out, double* C, int32_t* newton_iters,
+                             uint8_t* status, uint32_t* flags, void* stream) {
+    AM_TRY(check_law(law));
+    AM_TRY(check_cfg(cfg));
+    if (B < 0) return fail(AM_ERR_ARG, "negative batch size");
+    const int m = law_m(law);
+    if (B > 0 && (!eps_n || !eps_np1 || !sigma || (m && (!a_n || !a_out)) || (want_tangent && !C)))
+        return fail(AM_ERR_ARG, "missing array argument");
+    KArgs k{};
+    k.B = B; k.gidx = nullptr;
+    k.eps_n = eps_n; k.a_n = a_n; k.eps_np1 = eps_np1; k.dt = dt; k.dt_scalar = dt_scalar;
+    k.le = {B, 1}; k.la = {B, 1}; k.lc = {B, 1};
+    k.sigma = sigma; k.a_out = a_out; k.C = want_tangent ? C : nullptr;
+    k.iters = newton_iters; k.status = status; k.flags = flags;
+    k.ncfg = newton_cfg(cfg);
+    return launch(law, k, (cudaStream_t)stream);
+}
+
+namespace {
+
+// Device staging for the host-pointer path: two slots so that chunk c+1's
+// copies overlap chunk c's kernel (the paper's two-stream staging,
+// PAPER.md:623, with device-resident buffers reused across calls).
+struct HostPipe {
+    static constexpr int kSlots = 2;
+    int device = -1;
+    int64_t cap = 0;
+    cudaStream_t stream[kSlots] = {};
+    double* in[kSlots] = {};     // eps_n | a_n | eps_np1 | dt
+    double* out[kSlots] = {};    // sigma | a_out | C
+    int32_t* iters[kSlots] = {};
+    uint8_t* status[kSlots] = {};
+    uint32_t* flags = nullptr;   // kSlots words
+    std::mutex mu;
+
+    int ensure(int64_t chunk) {
+        int dev;
+        AM_CUDA(cudaGetDevice(&dev));
+        if (dev == device && chunk <= cap) return AM_OK;
+        release();
+        device = dev;
+        for (int s = 0; s < kSlots; ++s) {
+            AM_CUDA(cudaStreamCreateWithFlags(&stream[s], cudaStreamNonBlocking));
+            AM_CUDA(cudaMalloc(&in[s], sizeof(double) * chunk * 20));
+            AM_CUDA(cudaMalloc(&out[s], sizeof(double) * chunk * 49));
+            AM_CUDA(cudaMalloc(&iters[s], sizeof(int32_t) * chunk));
+            AM_CUDA(cudaMalloc(&status[s], chunk));
+        }
+        AM_CUDA(cudaMalloc(&flags, sizeof(uint32_t) * kSlots));
+        cap = chunk;
+        return AM_OK;
+    }
+    void release() {
+        if (device < 0) return;
+        for (int s = 0; s < kSlots; ++s) {
+            cudaFree(in[s]); cudaFree(out[s]); cudaFree(iters[s]); cudaFree(status[s]);
+            if (stream[s]) cudaStreamDestroy(stream[s]);
+            in[s] = out[s] = nullptr; iters[s] = nullptr; status[s] = nullptr; stream[s] = nullptr;
+        }
+        cudaFree(flags);
+        flags = nullptr;
+        cap = 0;
+        device = -1;
+    }
+};
+
+HostPipe& host_pipe() {
+    static HostPipe p;
+    return p;
+}
+
+}  // namespace
+
+extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t B, const double* eps_n,
+                                  const double* a_n, const double* eps_np1, const double* dt, int want_tangent,
+                                  double* sigma, double* a_out, double* C, int32_t* newton_iters, uint8_t* status) {
+    AM_TRY(check_law(law));
+    AM_TRY(check_cfg(cfg));
+    if (B < 0) return fail(AM_ERR_ARG, "negative batch size");
+    if (B == 0) return AM_OK;
+    const int m = law_m(law);
+    if (!eps_n || !eps_np1 || !dt || !sigma || (m && (!a_n || !a_out)) || (want_tangent && !C))
+        return fail(AM_ERR_ARG, "missing array argument");
+    HostPipe& P = host_pipe();
+    std::lock_guard<std::mutex> lock(P.mu);
+    const int64_t chunk = B < (int64_t(1) << 18) ? B : (int64_t(1) << 18);
+    AM_TRY(P.ensure(chunk));
+    AM_CUDA(cudaMemsetAsync(P.flags, 0, sizeof(uint32_t) * HostPipe::kSlots, P.stream[0]));
+    AM_CUDA(cudaStreamSynchronize(P.stream[0]));
+    const int64_t nchunks = (B + chunk - 1) / chunk;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int s = int(c % HostPipe::kSlots);
+        cudaStream_t st = P.stream[s];
+        const int64_t lo = c * chunk, n = (B - lo) < chunk ? (B - lo) : chunk;
+        double* d_en = P.in[s];
+        double* d_an = d_en + 6 * n;
+        double* d_e1 = d_an + 7 * n;
+        double* d_dt = d_e1 + 6 * n;
+        double* d_sig = P.out[s];
+        double* d_ao = d_sig + 6 * n;
+        double* d_C = d_ao + 7 * n;
+        AM_CUDA(cudaMemcpyAsync(d_en, eps_n + 6 * lo, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, st));
+        if (m) AM_CUDA(cudaMemcpyAsync(d_an, a_n + m * lo, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
+        AM_CUDA(cudaMemcpyAsync(d_e1, eps_np1 + 6 * lo, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, st));
+        AM_CUDA(cudaMemcpyAsync(d_dt, dt + lo, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        KArgs k{};
+        k.B = n; k.gidx = nullptr;
+        k.eps_n = d_en; k.a_n = d_an; k.eps_np1 = d_e1; k.dt = d_dt; k.dt_scalar = 0.0;
+        k.le = {1, 6}; k.la = {1, m}; k.lc = {1, 36};
+        k.sigma = d_sig; k.a_out = d_ao; k.C = want_tangent ? d_C : nullptr;
+        k.iters = P.iters[s]; k.status = P.status[s]; k.flags = P.flags + s;
+        k.ncfg = newton_cfg(cfg);
+        AM_TRY(launch(law, k, st));
+        AM_CUDA(cudaMemcpyAsync(sigma + 6 * lo, d_sig, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, st));
+        if (m) AM_CUDA(cudaMemcpyAsync(a_out + m * lo, d_ao, sizeof(double) * m * n, cudaMemcpyDeviceToHost, st));
+        if (want_tangent)
+            AM_CUDA(cudaMemcpyAsync(C + 36 * lo, d_C, sizeof(double) * 36 * n, cudaMemcpyDeviceToHost, st));
+        if (newton_iters)
+            AM_CUDA(cudaMemcpyAsync(newton_iters + lo, P.iters[s], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+        if (status) AM_CUDA(cudaMemcpyAsync(status + lo, P.status[s], n, cudaMemcpyDeviceToHost, st));
+    }
+    uint32_t flags[HostPipe::kSlots];
+    AM_CUDA(cudaMemcpyAsync(flags, P.flags, sizeof(flags), cudaMemcpyDeviceToHost, P.stream[0]));
+    for (int s = 0; s < HostPipe::kSlots; ++s) AM_CUDA(cudaStreamSynchronize(P.stream[s]));
+    uint32_t any = 0;
+    for (int s = 0; s < HostPipe::kSlots; ++s) any |= flags[s];
+    if (any & AM_VOXEL_NEWTON_FAILED)
+        return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
+    if (any & AM_VOXEL_SINGULAR) return fail(AM_ERR_SINGULAR, "pivot below 1e-14 * max|A|");
+    return AM_OK;
+}
+
+extern "C" int am_constitutive_host(const am_law* law, int64_t B, const double* eps, const double* a,
+                                    double* sigma, double* A, double* f, double* dfda, double* dfde) {
+    AM_TRY(check_law(law));
+    if (B <= 0) return B == 0 ? AM_OK : fail(AM_ERR_ARG, "negative batch size");
+    const int m = law_m(law);
+    const size_t n_in = 6 + m, n_out = 6 + m + m + m * m + 6 * m;
+    double *d_in, *d_out;
+    AM_CUDA(cudaMalloc(&d_in, sizeof(double) * n_in * B));
+    AM_CUDA(cudaMalloc(&d_out, sizeof(double) * n_out * B));
+    double* d_e = d_in;
+    double* d_a = d_in + 6 * B;
+    double* d_s = d_out;
+    double* d_A = d_s + 6 * B;
+    double* d_f = d_A + m * B;
+    double* d_J = d_f + m * B;
+    double* d_Je = d_J + m * m * B;
+    int rc = AM_OK;
+    cudaError_t e = cudaMemcpy(d_e, eps, sizeof(double) * 6 * B, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && m) e = cudaMemcpy(d_a, a, sizeof(double) * m * B, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        const unsigned blocks = unsigned((B + 127) / 128);
+        if (law->kind == AM_LAW_MICHEL_SUQUET) {
+            auto L = MichelSuquetLaw::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot, law->sigma_d, law->n);
+            k_constitutive<<<blocks, 128>>>(L, B, d_e, d_a, d_s, d_A, d_f, d_J, d_Je);
+        } else {
+            auto L = LinearElasticLaw::make(law->E, law->nu);
+            k_constitutive<<<blocks, 128>>>(L, B, d_e, d_a, d_s, d_A, d_f, d_J, d_Je);
+        }
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && sigma) e = cudaMemcpy(sigma, d_s, sizeof(double) * 6 * B, cudaMemcpyDeviceToHost);
+    if (m) {
+        if (e == cudaSuccess && A) e = cudaMemcpy(A, d_A, sizeof(double) * m * B, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && f) e = cudaMemcpy(f, d_f, sizeof(double) * m * B, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && dfda) e = cudaMemcpy(dfda, d_J, sizeof(double) * m * m * B, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && dfde) e = cudaMemcpy(dfde, d_Je, sizeof(double) * 6 * m * B, cudaMemcpyDeviceToHost);
+    }
+    if (e != cudaSuccess) rc = fail(AM_ERR_CUDA, "am_constitutive_host: %s", cudaGetErrorString(e));
+    cudaFree(d_in);
+    cudaFree(d_out);
+    return rc;
+}

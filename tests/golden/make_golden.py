@@ -1,0 +1,363 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE.
+
+Run in the build container only (the reference tree does not exist on the
+GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [--skip-slow]
+
+Every fixture is produced by importing ``gsmkit`` from
+/root/reference/pkg/src and calling its public API unchanged, with
+``StrategyConfig(strategy="automatic", integrator="implicit-euler")``
+unless stated. Per-voxel Newton iteration counts are taken with a wrapper
+around ``MaterialStepProblem.rhs_and_jac`` that counts the compacted
+indices the Newton loop passes (odeint.py:376-377); the tangent
+post-process calls it with idx=None (odeint.py:421) and is not counted.
+"""
+
+import argparse
+import importlib.util
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.dont_write_bytecode = True
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+from gsmkit import gsm, linalg, odeint  # noqa: E402
+from gsmkit import homogenize as H  # noqa: E402
+from gsmkit.evaluator import StrategyConfig, evaluate_arrays  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_spec = importlib.util.spec_from_file_location(
+    "workloads", os.path.join(HERE, "..", "..", "paper_2006_04391_b200", "workloads.py")
+)
+W = importlib.util.module_from_spec(_spec)
+_spec.loader.exec_module(W)
+
+AUTO = StrategyConfig(strategy="automatic", integrator="implicit-euler")
+AUTO_STRESS = StrategyConfig(strategy="automatic", integrator="implicit-euler", error_measure="stress")
+CONV = StrategyConfig(strategy="conventional", integrator="implicit-euler")
+
+# ---------------------------------------------------------------- counters
+_COUNT = {"arr": None}
+_orig_rhs_and_jac = odeint.MaterialStepProblem.rhs_and_jac
+
+
+def _counting_rhs_and_jac(self, t, y, idx=None):
+    if idx is not None and _COUNT["arr"] is not None:
+        np.add.at(_COUNT["arr"], idx, 1)
+    return _orig_rhs_and_jac(self, t, y, idx)
+
+
+odeint.MaterialStepProblem.rhs_and_jac = _counting_rhs_and_jac
+
+
+def eval_counted(law, cfg, eps_n, a_n, eps_np1, dt, want_tangent):
+    """evaluate_arrays with per-voxel Newton counts (single chunk)."""
+    B = eps_np1.shape[0]
+    cfg = StrategyConfig(
+        strategy=cfg.strategy,
+        integrator=cfg.integrator,
+        error_measure=cfg.error_measure,
+        chunk_size=max(B, 1),
+    )
+    _COUNT["arr"] = np.zeros(B, dtype=np.int64)
+    try:
+        r = evaluate_arrays(law, cfg, eps_n, a_n, eps_np1, dt, want_tangent=want_tangent)
+        err = ""
+    except Exception as exc:  # noqa: BLE001
+        r = None
+        err = type(exc).__name__
+    cnt = _COUNT["arr"]
+    _COUNT["arr"] = None
+    frozen = np.broadcast_to(np.asarray(dt, dtype=float), (B,)) == 0.0
+    if frozen.any() and not frozen.all():
+        # the mixed split (evaluator.py:151-156) re-enters _evaluate_chunk on
+        # the dt > 0 subset, so the Newton indices are local to that subset
+        ipos = np.flatnonzero(~frozen)
+        full = np.zeros(B, dtype=np.int64)
+        full[ipos] = cnt[: len(ipos)]
+        cnt = full
+    return r, cnt, err
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {name} ({os.path.getsize(path) / 1024:.1f} KiB)")
+
+
+# ---------------------------------------------------------------- material
+def make_material():
+    law = gsm.MichelSuquet()
+    eps_n, a_n, eps_np1, dt = W.config2_batch(1024, seed=0)
+    r, cnt, err = eval_counted(law, AUTO, eps_n, a_n, eps_np1, dt, True)
+    assert not err
+    rs, cnts, errs = eval_counted(law, AUTO_STRESS, eps_n, a_n, eps_np1, dt, False)
+    assert not errs
+    save(
+        "material_evp.npz",
+        eps_n=eps_n, a_n=a_n, eps_np1=eps_np1, dt=dt,
+        sigma=r.sigma, a=r.a, C=r.C, iters=cnt,
+        sigma_stress=rs.sigma, a_stress=rs.a, iters_stress=cnts,
+    )
+
+    # edge cases, one law call per case (the reference raises per call)
+    rng = np.random.default_rng(7)
+    cases = {}
+
+    # elastic voxels: tiny strains, zero state -> one Newton iteration each
+    B = 64
+    en = rng.normal(0, 1e-6, (B, 6)); ep = en + rng.normal(0, 1e-6, (B, 6)); an = np.zeros((B, 7))
+    cases["elastic"] = (en, an, ep, np.full(B, 0.05))
+
+    # frozen mix: every third voxel has dt == 0 (evaluator.py:142-170)
+    en, an, ep, dtv = W.config2_batch(48, seed=11)
+    dtv[::3] = 0.0
+    cases["frozen_mix"] = (en, an, ep, dtv)
+
+    # all frozen
+    en, an, ep, dtv = W.config2_batch(16, seed=12)
+    cases["frozen_all"] = (en, an, ep, np.zeros(16))
+
+    # negative alpha on input: clamp_state (gsm.py:252-256) after integration
+    en, an, ep, dtv = W.config2_batch(32, seed=13)
+    an[:, 6] = -np.abs(an[:, 6])
+    ep[:16] = en[:16] + 1e-7  # elastic half keeps a_n, clamp shows
+    cases["clamp"] = (en, an, ep, dtv)
+
+    # large increments, long steps: many Newton iterations
+    en = np.zeros((64, 6)); ep = rng.normal(0, 1.0, (64, 6)); an = np.zeros((64, 7))
+    cases["large"] = (en, an, ep, np.full(64, 1.0))
+
+    # varied dt per voxel
+    en, an, ep, dtv = W.config2_batch(64, seed=14)
+    dtv = 10.0 ** rng.uniform(-4, 2, 64)
+    cases["dt_sweep"] = (en, an, ep, dtv)
+
+    # Newton failure: singular iteration matrix at huge h (odeint.py:380-381)
+    en = np.zeros((4, 6)); ep = np.random.default_rng(1).normal(0, 1.0, (4, 6)); an = np.zeros((4, 7))
+    cases["newton_fail"] = (en, an, ep, np.full(4, 1e6))
+
+    out = {}
+    for name, (en, an, ep, dtv) in cases.items():
+        for tang in (False, True):
+            r, cnt, err = eval_counted(law, AUTO, en, an, ep, dtv, tang)
+            tag = f"{name}_{'t' if tang else 'n'}"
+            out[f"{tag}_eps_n"] = en
+            out[f"{tag}_a_n"] = an
+            out[f"{tag}_eps_np1"] = ep
+            out[f"{tag}_dt"] = dtv
+            out[f"{tag}_err"] = np.array(err)
+            out[f"{tag}_iters"] = cnt
+            if r is not None:
+                out[f"{tag}_sigma"] = r.sigma
+                out[f"{tag}_a"] = r.a
+                if tang:
+                    out[f"{tag}_C"] = r.C
+    out["cases"] = np.array(sorted(cases))
+
+    # linear elastic laws (m == 0 path, evaluator.py:134-140)
+    for lname, law_le in (("le_matrix", gsm.LinearElastic(55e9, 0.33)), ("le_fiber", gsm.LinearElastic(300e9, 0.25))):
+        B = 64
+        en = rng.normal(0, 1e-3, (B, 6)); ep = en + rng.normal(0, 1e-3, (B, 6))
+        an = np.zeros((B, 0))
+        r, _, err = eval_counted(law_le, AUTO, en, an, ep, np.full(B, 0.05), True)
+        assert not err
+        out[f"{lname}_eps_n"] = en
+        out[f"{lname}_eps_np1"] = ep
+        out[f"{lname}_sigma"] = r.sigma
+        out[f"{lname}_C"] = r.C
+    save("material_edge.npz", **out)
+
+
+# ---------------------------------------------------------------- constitutive
+def make_constitutive():
+    law = gsm.MichelSuquet()
+    rng = np.random.default_rng(3)
+    B = 256
+    eps = rng.normal(0, 2e-3, (B, 6))
+    a = np.zeros((B, 7))
+    a[:, :6] = rng.normal(0, 5e-4, (B, 6))
+    a[:, 6] = np.abs(rng.normal(0, 1e-3, B))
+    a[:8] = 0.0
+    eps[:4] = 0.0  # elastic states -> zero flow, zero Jacobians
+    # The reference's batched generalized_stress fails to stack the scalar
+    # A_alpha = -sigma_Y (gsm.py:50, 441-449); evaluate point by point.
+    def per_point(fn):
+        return np.stack([np.asarray(fn(law, eps[i], a[i]), dtype=float) for i in range(B)])
+
+    save(
+        "constitutive.npz",
+        eps=eps, a=a,
+        stress=per_point(gsm.stress),
+        gen_stress=per_point(gsm.generalized_stress),
+        rhs=per_point(gsm.evolution_rhs),
+        dfda=per_point(gsm.rhs_jacobian),
+        dfde=per_point(gsm.rhs_strain_jacobian),
+        le_stress=gsm.stress(gsm.LinearElastic(300e9, 0.25), eps, np.zeros((B, 0))),
+    )
+
+
+# ---------------------------------------------------------------- fourier
+def make_fourier():
+    rng = np.random.default_rng(5)
+    out = {}
+    dims_list = [(8, 8, 8), (16, 12, 10), (9, 8, 7), (4, 6, 5), (1, 8, 6)]
+    ref = H.ReferenceMaterial(lam=80068553737.28441, mu=70338345864.66165)
+    for k, dims in enumerate(dims_list):
+        tau = rng.normal(0, 1e8, (6,) + dims)
+        sig = rng.normal(0, 1e8, (6,) + dims) + np.array([3e8, 1e8, -2e8, 1e7, 0, 5e6])[:, None, None, None]
+        eps = rng.normal(0, 1e-3, (6,) + dims)
+        out[f"d{k}_dims"] = np.array(dims)
+        out[f"d{k}_tau"] = tau
+        out[f"d{k}_green"] = H.GreenOperator(dims, ref).apply(tau)
+        out[f"d{k}_sig"] = sig
+        out[f"d{k}_residual"] = np.array(H.equilibrium_residual(sig))
+        out[f"d{k}_eps"] = eps
+        out[f"d{k}_iso"] = H.apply_isotropic(ref, eps)
+    out["ndims"] = np.array(len(dims_list))
+    out["ref"] = np.array([ref.lam, ref.mu])
+
+    # reference_update on random tangent fields (homogenize.py:307-329)
+    for k in range(3):
+        N = 300
+        law = gsm.MichelSuquet()
+        C = np.broadcast_to(law.Ce, (N, 6, 6)).copy()
+        C += rng.normal(0, 5e9, (N, 6, 6))
+        out[f"ru{k}_C"] = C
+        r = H.reference_update(C)
+        out[f"ru{k}_lam_mu"] = np.array([r.lam, r.mu])
+    save("fourier.npz", **out)
+
+
+# ---------------------------------------------------------------- config 1
+def make_config1():
+    n = 32
+    ids = W.sphere_ids(n)
+    out = {"ids": ids}
+    sub = np.arange(0, n**3, 37)
+    out["sub"] = sub
+    for tag, free in (("strain", np.zeros(6, dtype=bool)), ("mixed", np.array([False] + [True] * 5))):
+        grid = H.VoxelGrid(ids, [gsm.LinearElastic(55e9, 0.33), gsm.LinearElastic(300e9, 0.25)])
+        hom = H.Homogenizer(grid, AUTO)
+        eb = np.zeros(6); eb[0] = 1e-3
+        t0 = time.time()
+        eps, sig, info = hom.solve_step(eb, 1.0, free_mask=free)
+        print(f"config1 {tag}: {info.iterations} it, {time.time() - t0:.2f}s")
+        out[f"{tag}_iters"] = np.array(info.iterations)
+        out[f"{tag}_history"] = np.array(info.history)
+        out[f"{tag}_sig_bar"] = sig.mean(axis=(1, 2, 3))
+        out[f"{tag}_eps_bar"] = eps.mean(axis=(1, 2, 3))
+        out[f"{tag}_sig_sub"] = sig.reshape(6, -1)[:, sub]
+        out[f"{tag}_eps_sub"] = eps.reshape(6, -1)[:, sub]
+        out[f"{tag}_ref"] = np.array([hom.reference.lam, hom.reference.mu])
+    # SolverError: iteration cap with history (homogenize.py:466-471)
+    grid = H.VoxelGrid(ids, [gsm.LinearElastic(55e9, 0.33), gsm.LinearElastic(300e9, 0.25)])
+    hom = H.Homogenizer(grid, AUTO, max_iterations=4)
+    eb = np.zeros(6); eb[0] = 1e-3
+    try:
+        hom.solve_step(eb, 1.0)
+        raise AssertionError("expected SolverError")
+    except H.SolverError as exc:
+        out["cap_history"] = np.array(exc.history)
+    save("config1.npz", **out)
+
+
+# ---------------------------------------------------------------- loading paths
+def _records_to_arrays(recs):
+    return dict(
+        step=np.array([r["step"] for r in recs]),
+        time=np.array([r["time"] for r in recs]),
+        eps_xx=np.array([r["eps_xx"] for r in recs]),
+        sig=np.stack([r["sig"] for r in recs]),
+        C11=np.array([r["C11"] for r in recs]),
+        C12=np.array([r["C12"] for r in recs]),
+        iterations=np.array([r["iterations"] for r in recs]),
+        mean_substeps=np.array([r["mean_substeps"] for r in recs]),
+    )
+
+
+def make_path8():
+    """8^3 toy MMC, 6 of 20 steps, fully automatic route, plus final state."""
+    grid = H.toy_mmc_grid(8)
+    path = H.LoadingPath(steps=20)
+    t0 = time.time()
+    # run the loop by hand to stop after 6 steps and keep the state
+    hom = H.Homogenizer(grid, AUTO)
+    times = path.times()
+    targets = path.eps_xx(times)
+    free = np.array([False, True, True, True, True, True])
+    recs = []
+    refs = [(hom.reference.lam, hom.reference.mu)]
+    for k in range(1, 7):
+        dt = times[k] - times[k - 1]
+        eb = np.zeros(6); eb[0] = targets[k]
+        eps, sigma, info = hom.solve_step(eb, dt, free_mask=free)
+        ebar = eps.mean(axis=(1, 2, 3))
+        _, C_vox, _, _ = hom.evaluate_field(eps, dt, want_tangent=True)
+        C_bar = C_vox.mean(axis=0)
+        hom.commit_step(eps, ebar)
+        hom.set_reference(H.reference_update(C_vox))
+        refs.append((hom.reference.lam, hom.reference.mu))
+        recs.append({"step": k, "time": float(times[k]), "eps_xx": float(ebar[0]), "sig": sigma.mean(axis=(1, 2, 3)),
+                     "C11": float(C_bar[0, 0]), "C12": float(C_bar[0, 1]), "iterations": info.iterations,
+                     "mean_substeps": info.mean_substeps, "Cbar": C_bar, "history": info.history})
+        print(f"path8 step {k}: {info.iterations} it ({time.time() - t0:.1f}s)")
+    arr = _records_to_arrays(recs)
+    arr["Cbar"] = np.stack([r["Cbar"] for r in recs])
+    hist = [np.array(r["history"]) for r in recs]
+    arr["history_flat"] = np.concatenate(hist)
+    arr["refs"] = np.array(refs)
+    arr["ids"] = grid.material_ids
+    arr["eps_n"] = hom.eps_n
+    arr["state0"] = grid.state[0]
+    save("path8_auto.npz", **arr)
+
+
+def make_path16_conv():
+    """16^3 toy MMC, 20 steps, per-law conventional oracle."""
+    _ea = H.evaluate_arrays
+
+    def _per_law(law, cfg, *a, **k):
+        if cfg.strategy == "conventional" and not law.has_conventional:
+            cfg = AUTO
+        return _ea(law, cfg, *a, **k)
+
+    H.evaluate_arrays = _per_law
+    try:
+        t0 = time.time()
+        grid = H.toy_mmc_grid(16)
+        recs = H.run_loading_path(grid, H.LoadingPath(steps=20), CONV)
+        print(f"path16 conventional: {time.time() - t0:.1f}s")
+    finally:
+        H.evaluate_arrays = _ea
+    arr = _records_to_arrays(recs)
+    arr["ids"] = grid.material_ids
+    save("path16_conv.npz", **arr)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--skip-slow", action="store_true")
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    jobs = {
+        "material": make_material,
+        "constitutive": make_constitutive,
+        "fourier": make_fourier,
+        "config1": make_config1,
+        "path16": make_path16_conv,
+        "path8": make_path8,
+    }
+    for name, fn in jobs.items():
+        if args.only and name not in args.only.split(","):
+            continue
+        if args.skip_slow and name in ("path8",):
+            continue
+        t0 = time.time()
+        fn()
+        print(f"[{name}] {time.time() - t0:.1f}s")

@@ -1,0 +1,62 @@
+"""Device material code (csrc/material.cuh) compiled for the host vs the reference fixtures.
+
+Same tolerances as the GPU parity tests; this runs on CPU so the AD /
+Newton / tangent logic is checked every round without a GPU.
+"""
+
+import numpy as np
+import pytest
+
+import _hostcheck as HC
+from conftest import golden
+from oracle import material as OM
+from _util import TOL_STATE, TOL_TANGENT, assert_close
+
+
+@pytest.mark.parametrize("tangent", [False, True])
+def test_config2(tangent):
+    g = golden("material_evp.npz")
+    r = HC.evaluate(OM.ALUMINUM, g["eps_n"], g["a_n"], g["eps_np1"], g["dt"], tangent)
+    assert r["code"] == 0
+    assert np.array_equal(r["iters"], g["iters"])
+    assert_close(r["sigma"], g["sigma"], TOL_STATE, "sigma")
+    assert_close(r["a"], g["a"], TOL_STATE, "a")
+    if tangent:
+        assert_close(r["C"], g["C"], TOL_TANGENT, "C")
+
+
+def test_stress_mode():
+    g = golden("material_evp.npz")
+    r = HC.evaluate(OM.ALUMINUM, g["eps_n"], g["a_n"], g["eps_np1"], g["dt"], False, newton_mode=1)
+    assert np.array_equal(r["iters"], g["iters_stress"])
+    assert_close(r["a"], g["a_stress"], TOL_STATE)
+
+
+@pytest.mark.parametrize("case", [str(c) for c in golden("material_edge.npz")["cases"]])
+@pytest.mark.parametrize("t", ["n", "t"])
+def test_edge(case, t):
+    g = golden("material_edge.npz")
+    tag = f"{case}_{t}"
+    r = HC.evaluate(OM.ALUMINUM, g[tag + "_eps_n"], g[tag + "_a_n"], g[tag + "_eps_np1"], g[tag + "_dt"], t == "t")
+    assert np.array_equal(r["iters"], g[tag + "_iters"])
+    if str(g[tag + "_err"]) == "NewtonDivergenceError":
+        assert r["code"] & 1
+        return
+    assert r["code"] == 0
+    assert_close(r["sigma"], g[tag + "_sigma"], TOL_STATE)
+    assert_close(r["a"], g[tag + "_a"], TOL_STATE)
+    if t == "t":
+        assert_close(r["C"], g[tag + "_C"], TOL_TANGENT)
+
+
+def test_against_oracle_random():
+    """Larger seeded batch: host build of the kernel vs the C oracle."""
+    from paper_2006_04391_b200.workloads import config2_batch
+
+    en, an, ep, dt = config2_batch(4096, seed=123)
+    r = HC.evaluate(OM.ALUMINUM, en, an, ep, dt, True)
+    o = OM.evaluate(OM.ALUMINUM, en, an, ep, dt, True, threads=4)
+    assert np.array_equal(r["iters"], o["iters"])
+    assert_close(r["sigma"], o["sigma"], TOL_STATE)
+    assert_close(r["a"], o["a"], TOL_STATE)
+    assert_close(r["C"], o["C"], TOL_TANGENT)
