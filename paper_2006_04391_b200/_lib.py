@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libautomat.so")
+# AM_LIB overrides the library path (kernel-variant experiments under tools/)
+LIB_PATH = os.environ.get("AM_LIB") or os.path.join(HERE, "libautomat.so")
 
 AM_OK = 0
 AM_ERR_CONFIG = 1

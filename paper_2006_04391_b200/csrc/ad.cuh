@@ -187,6 +187,31 @@ AM_HD D<A> dpow(const D<A>& x, double c) {
     const double f = c * ::pow(x.v, c - 1.0);
     return map_d(x, ::pow(x.v, c), [=](double p) { return f * p; });
 }
+// Value and local partial of a constant-exponent power node as duals:
+// val = x^c (dual), dval = c * x^(c-1) (dual, i.e. including c(c-1)x^(c-2)dx).
+// One pow(x, c-2) yields all three powers (x^(c-1) = x^(c-2)*x, x^c =
+// x^(c-1)*x) whenever that is exact in the limit: x > 0, or c >= 2 (x = 0
+// gives 0^(c-2) in {0, 1} and zero higher powers).  Otherwise the powers are
+// taken separately like Dual1.__pow__ (ad.py:99-100).  Relative difference
+// to separate pow() calls: a few ulp.
+template <uint32_t A>
+AM_HD void powjet(const D<A>& x, double c, D<A>& val, D<A>& dval) {
+    double p0, p1, p2;
+    if (x.v > 0.0 || c >= 2.0) {
+        p2 = ::pow(x.v, c - 2.0);
+        p1 = p2 * x.v;
+        p0 = p1 * x.v;
+    } else {
+        p0 = ::pow(x.v, c);
+        p1 = ::pow(x.v, c - 1.0);
+        p2 = ::pow(x.v, c - 2.0);
+    }
+    const double f1 = c * p1;            // d/dx x^c
+    const double f2 = c * ((c - 1.0) * p2);  // d/dx (c x^(c-1))
+    val = map_d(x, p0, [=](double p) { return f1 * p; });
+    dval = map_d(x, f1, [=](double p) { return f2 * p; });
+}
+
 template <uint32_t A>
 AM_HD D<A> dsqrt(const D<A>& x) {
     const double s = ::sqrt(x.v);
@@ -252,8 +277,10 @@ template <class A, class B>
 struct Div : Node { A a; B b; };
 template <class A>
 struct Neg : Node { A a; };
-template <class A>
-struct Pow : Node { A a; double c; };
+// Pow caches its primal value and local partial c*x^(c-1) (both as duals)
+// at construction: one pow() serves v() and back() (see powjet).
+template <class A, class VT>
+struct Pow : Node { A a; double c; VT val, dval; };
 template <class A>
 struct Sqrt : Node { A a; };
 template <class A>
@@ -295,7 +322,12 @@ AM_BIN(/, Div)
 template <class A, std::enable_if_t<is_node<A>, int> = 0>
 AM_HD Neg<A> operator-(const A& a) { Neg<A> n; n.a = a; return n; }
 template <class A, std::enable_if_t<is_node<A>, int> = 0>
-AM_HD Pow<A> npow(const A& a, double c) { Pow<A> n; n.a = a; n.c = c; return n; }
+AM_HD auto npow(const A& a, double c) {
+    using VT = std::decay_t<decltype(v(a))>;
+    Pow<A, VT> n; n.a = a; n.c = c;
+    powjet(v(a), c, n.val, n.dval);
+    return n;
+}
 #define AM_UN(fn, NODE) \
     template <class A, std::enable_if_t<is_node<A>, int> = 0> AM_HD NODE<A> fn(const A& a) { NODE<A> n; n.a = a; return n; }
 AM_UN(nsqrt, Sqrt)
@@ -320,8 +352,8 @@ template <class A, class B>
 AM_HD auto v(const Div<A, B>& n) { return v(n.a) / v(n.b); }
 template <class A>
 AM_HD auto v(const Neg<A>& n) { return -v(n.a); }
-template <class A>
-AM_HD auto v(const Pow<A>& n) { return dpow(v(n.a), n.c); }
+template <class A, class VT>
+AM_HD const VT& v(const Pow<A, VT>& n) { return n.val; }
 template <class A>
 AM_HD auto v(const Sqrt<A>& n) { return dsqrt(v(n.a)); }
 template <class A>
@@ -348,8 +380,8 @@ template <int I, class A, class B>
 struct has<I, Div<A, B>> : std::bool_constant<has<I, A>::value || has<I, B>::value> {};
 template <int I, class A>
 struct has<I, Neg<A>> : has<I, A> {};
-template <int I, class A>
-struct has<I, Pow<A>> : has<I, A> {};
+template <int I, class A, class VT>
+struct has<I, Pow<A, VT>> : has<I, A> {};
 template <int I, class A>
 struct has<I, Sqrt<A>> : has<I, A> {};
 template <int I, class A>
@@ -397,10 +429,10 @@ AM_HD auto adj(const Div<A, B>& n, const BV& bv) {
 }
 template <int I, class A, class BV>
 AM_HD auto adj(const Neg<A>& n, const BV& bv) { return adjl<I>(n.a, [&] { return -bv; }); }
-// RPow.back: bv * (c * av**(c-1))
-template <int I, class A, class BV>
-AM_HD auto adj(const Pow<A>& n, const BV& bv) {
-    return adjl<I>(n.a, [&] { return bv * (plain(n.c) * dpow(v(n.a), n.c - 1.0)); });
+// RPow.back: bv * (c * av**(c-1)), the partial cached by powjet
+template <int I, class A, class VT, class BV>
+AM_HD auto adj(const Pow<A, VT>& n, const BV& bv) {
+    return adjl<I>(n.a, [&] { return bv * n.dval; });
 }
 // RSqrt.back: bv * (0.5 / sqrt(av))
 template <int I, class A, class BV>

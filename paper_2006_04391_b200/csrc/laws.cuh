@@ -51,6 +51,12 @@ struct MichelSuquetLaw {
     static constexpr int m = 7;
     double lam, mu, H, sigma_Y, eps0_dot, sigma_d, n;
 
+#ifdef __CUDA_ARCH__
+    __device__ void launder() {
+        asm volatile("" : "+d"(lam), "+d"(mu), "+d"(H), "+d"(sigma_Y), "+d"(eps0_dot), "+d"(sigma_d), "+d"(n));
+    }
+#endif
+
     AM_HD static MichelSuquetLaw make(double E, double nu, double sigma_Y, double H, double eps0_dot,
                                       double sigma_d, double n) {
         MichelSuquetLaw L;

@@ -41,46 +41,116 @@ struct KArgs {
     NewtonCfg ncfg;
 };
 
-template <class Law>
-__global__ void __launch_bounds__(128) k_material(Law L, KArgs k) {
-    constexpr int m = Law::m;
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
+// writes C[i][j] of item `off` to C[(i * 6 + j) * cs + off]
+struct GlobalSink {
+    double* C;
+    int64_t cs, off;
+    bool finite = true;
+    __device__ void col(int j, const double* c) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            C[(i * 6 + j) * cs + off] = c[i];
+            finite = finite && (c[i] - c[i] == 0.0);
+        }
+    }
+};
+
+// K1: one thread per material point, grid-stride, all intermediates in
+// registers.  Two phases (material.cuh):
+//   k_material<Law, Mode, Raw>  Newton (+ clamp + stress unless Raw).  With
+//                               Raw the unclamped state goes to a_out for
+//                               the tangent phase.
+//   k_tangent<Law>              tangent post-process + clamp + stress + C.
+// Mode = Newton convergence measure; each combination is its own
+// instantiation so the hot Newton loop carries no dead code
+// (instruction-cache footprint).  The Newton kernel runs best at 4 CTAs per
+// SM (128 registers), the tangent kernel with the full 255-register budget
+// (tools/k1_variants.py measurements).
+#ifndef AM_K1_MINB_N
+#define AM_K1_MINB_N 4
+#endif
+#ifndef AM_K1_MINB_T
+#define AM_K1_MINB_T 1
+#endif
+
+struct PointIO {
+    const KArgs& k;
+    int64_t b, eo, ao;
+    __device__ PointIO(const KArgs& k_, int64_t b_) : k(k_), b(b_) {
         const int64_t g = k.gidx ? k.gidx[b] : b;
-        const int64_t eo = g * k.le.es, ao = b * k.la.es;
-        double en[6], e1[6], an[m > 0 ? m : 1], ao_[m > 0 ? m : 1], sig[6];
+        eo = g * k.le.es;
+        ao = b * k.la.es;
+    }
+    __device__ void eps(double* en, double* ep) const {
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
             en[c] = __ldg(k.eps_n + c * k.le.cs + eo);
-            e1[c] = __ldg(k.eps_np1 + c * k.le.cs + eo);
+            ep[c] = __ldg(k.eps_np1 + c * k.le.cs + eo);
         }
+    }
+    template <int m>
+    __device__ void load_a(const double* src, double* a) const {
 #pragma unroll
-        for (int c = 0; c < m; ++c) an[c] = __ldg(k.a_n + c * k.la.cs + ao);
-        const double dt = k.dt ? __ldg(k.dt + b) : k.dt_scalar;
-        int it = 0;
-        int st;
-        if (k.C) {
-            double C[6][6];
-            st = eval_voxel(L, k.ncfg, en, an, e1, dt, sig, ao_, C, it);
-            const int64_t co = b * k.lc.es;
-            bool fin = true;
+        for (int c = 0; c < m; ++c) a[c] = src[c * k.la.cs + ao];
+    }
+    template <int m>
+    __device__ void store_a(const double* a) const {
 #pragma unroll
-            for (int i = 0; i < 6; ++i)
-#pragma unroll
-                for (int j = 0; j < 6; ++j) {
-                    k.C[(i * 6 + j) * k.lc.cs + co] = C[i][j];
-                    fin = fin && (C[i][j] - C[i][j] == 0.0);
-                }
-            if (!fin) st |= ST_NONFINITE;
-        } else {
-            st = eval_voxel(L, k.ncfg, en, an, e1, dt, sig, ao_, (double(*)[6]) nullptr, it);
-        }
+        for (int c = 0; c < m; ++c) k.a_out[c * k.la.cs + ao] = a[c];
+    }
+    __device__ void store_sigma(const double* sig) const {
 #pragma unroll
         for (int c = 0; c < 6; ++c) k.sigma[c * k.le.cs + eo] = sig[c];
-#pragma unroll
-        for (int c = 0; c < m; ++c) k.a_out[c * k.la.cs + ao] = ao_[c];
-        if (k.iters) k.iters[b] = it;
+    }
+    __device__ double dt() const { return k.dt ? __ldg(k.dt + b) : k.dt_scalar; }
+    __device__ void status(int st) const {
         if (k.status) k.status[b] = (uint8_t)st;
         if (st && k.flags) atomicOr(k.flags, (uint32_t)st);
+    }
+};
+
+template <class Law, int Mode, bool Raw>
+__global__ void __launch_bounds__(128, AM_K1_MINB_N) k_material(Law L, KArgs k) {
+    constexpr int m = Law::m;
+    constexpr int ms = m > 0 ? m : 1;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
+        const PointIO io(k, b);
+        double en[6], ep[6], an[ms], a[ms];
+        io.eps(en, ep);
+        io.load_a<m>(k.a_n, an);
+        int it = 0;
+        const int st = newton_point<Law, Mode>(L, k.ncfg, en, an, ep, io.dt(), a, it);
+        if constexpr (Raw) {
+            io.store_a<m>(a);
+        } else {
+            double ac[ms], sig[6];
+            stress_point(L, ep, a, ac, sig);
+            io.store_sigma(sig);
+            io.store_a<m>(ac);
+        }
+        if (k.iters) k.iters[b] = it;
+        io.status(st);
+    }
+}
+
+// reads the unclamped state from a_out and the Newton status from status
+template <class Law>
+__global__ void __launch_bounds__(128, AM_K1_MINB_T) k_tangent(Law L, KArgs k) {
+    constexpr int m = Law::m;
+    constexpr int ms = m > 0 ? m : 1;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
+        const PointIO io(k, b);
+        double en[6], ep[6], a[ms], ac[ms], sig[6];
+        io.eps(en, ep);
+        if constexpr (m > 0) io.load_a<m>(k.a_out, a);
+        int st = (m > 0) ? k.status[b] : 0;
+        GlobalSink sink{k.C, k.lc.cs, b * k.lc.es};
+        if (st & ST_NEWTON) failed_point(L, ep, a, ac, sig, sink);
+        else st |= tangent_point(L, en, ep, io.dt(), a, ac, sig, sink);
+        if (!sink.finite) st |= ST_NONFINITE;
+        io.store_sigma(sig);
+        io.store_a<m>(ac);
+        io.status(st);
     }
 }
 
@@ -140,20 +210,46 @@ static int check_cfg(const am_cfg* cfg) {
 
 static NewtonCfg newton_cfg(const am_cfg* cfg) { return NewtonCfg{cfg->newton_mode, cfg->max_newton, cfg->newton_tol}; }
 
-static int launch(const am_law* law, const KArgs& k, cudaStream_t s) {
-    if (k.B == 0) return AM_OK;
+template <class Law>
+static int launch_law(const Law& L, KArgs k, cudaStream_t s) {
     const int threads = 128;
     int64_t blocks = (k.B + threads - 1) / threads;
     if (blocks > (int64_t)kSMs * 1024) blocks = (int64_t)kSMs * 1024;
-    if (law->kind == AM_LAW_MICHEL_SUQUET) {
-        auto L = MichelSuquetLaw::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot, law->sigma_d, law->n);
-        k_material<<<(unsigned)blocks, threads, 0, s>>>(L, k);
-    } else {
-        auto L = LinearElasticLaw::make(law->E, law->nu);
-        k_material<<<(unsigned)blocks, threads, 0, s>>>(L, k);
+    const unsigned g = (unsigned)blocks;
+    const bool stress = k.ncfg.mode == AM_NEWTON_STRESS;
+    if (!k.C) {
+        if (stress) k_material<Law, 1, false><<<g, threads, 0, s>>>(L, k);
+        else k_material<Law, 0, false><<<g, threads, 0, s>>>(L, k);
+        AM_CUDA(cudaGetLastError());
+        return AM_OK;
     }
+    // tangent: Newton (raw state) then the tangent phase; the Newton status
+    // travels through `status` (a stream-ordered scratch when the caller
+    // does not want it)
+    uint8_t* scratch = nullptr;
+    if (Law::m > 0 && !k.status) {
+        AM_CUDA(cudaMallocAsync((void**)&scratch, (size_t)k.B, s));
+        k.status = scratch;
+    }
+    if (Law::m > 0) {
+        KArgs kn = k;
+        kn.flags = nullptr;  // the tangent kernel reports the combined status
+        if (stress) k_material<Law, 1, true><<<g, threads, 0, s>>>(L, kn);
+        else k_material<Law, 0, true><<<g, threads, 0, s>>>(L, kn);
+        AM_CUDA(cudaGetLastError());
+    }
+    k_tangent<Law><<<g, threads, 0, s>>>(L, k);
     AM_CUDA(cudaGetLastError());
+    if (scratch) AM_CUDA(cudaFreeAsync(scratch, s));
     return AM_OK;
+}
+
+static int launch(const am_law* law, const KArgs& k, cudaStream_t s) {
+    if (k.B == 0) return AM_OK;
+    if (law->kind == AM_LAW_MICHEL_SUQUET)
+        return launch_law(
+            MichelSuquetLaw::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot, law->sigma_d, law->n), k, s);
+    return launch_law(LinearElasticLaw::make(law->E, law->nu), k, s);
 }
 
 int law_m(const am_law* law) { return law->kind == AM_LAW_MICHEL_SUQUET ? 7 : 0; }

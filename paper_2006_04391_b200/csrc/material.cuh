@@ -239,135 +239,412 @@ AM_HD double rms(const double* x) {
     return sqrt(s / N);
 }
 
-// ---------------------------------------------------------------- Newton
-// _newton_implicit_euler (odeint.py:357-401) for one voxel: solves
-// a - a0 - h f(eps(t1), a) = 0 from a = a0.  Returns ok; iters counts the
-// rhs_and_jac evaluations (the reference's per-voxel Newton count).
+
+#ifdef __CUDACC__
+#define AM_COLD __host__ __device__ __noinline__
+#else
+#define AM_COLD __attribute__((noinline))
+#endif
+
+// ---------------------------------------------------------------- Jacobian shape
+// The AD proves at compile time which columns of df/da are structurally
+// zero: the tangent mask of every f_i lacks them.  For the Michel-Suquet
+// law omega is linear in alpha, so A does not depend on a_6 and column 6
+// vanishes ("zero last column"); M = I - h J is then block
+// lower triangular [[D, 0], [R, I]] with a dense nd x nd block D.
+template <class FT, int... I>
+constexpr uint32_t tup_mask(std::integer_sequence<int, I...>) {
+    return (0u | ... | std::decay_t<decltype(get<I>(std::declval<FT&>()))>::mask);
+}
 template <class Law>
-AM_HD bool newton_ie(const Law& L, const NewtonCfg& cfg, const double* e1, double h, const double* a0,
-                     double* a, int& iters) {
-    constexpr int m = Law::m;
-    double res_prev = INFINITY;
-    int growth = 0;
-    double sig_prev[6];
-#pragma unroll
-    for (int i = 0; i < m; ++i) a[i] = a0[i];
-    if (cfg.mode == 1) stress_plain(L, e1, a, sig_prev);
-    iters = 0;
-    for (int pass = 0; pass < cfg.max_it; ++pass) {
-        ++iters;
-        double f[m], M[m][m], F[m], dl[m], an[m], sc[m];
-        int piv[m];
-        rhs_jac_a(L, e1, a, f, M);
-        bool finite = true;
-#pragma unroll
-        for (int i = 0; i < m; ++i) {
-            F[i] = a[i] - a0[i] - h * f[i];
-            finite = finite && (F[i] - F[i] == 0.0);  // isfinite
-        }
-#pragma unroll
-        for (int i = 0; i < m; ++i)
-#pragma unroll
-            for (int k = 0; k < m; ++k) M[i][k] = (i == k ? 1.0 : 0.0) - h * M[i][k];
-        const bool fac_ok = lu_factor(M, piv);
-        const bool bad = !fac_ok || !finite;
-#pragma unroll
-        for (int i = 0; i < m; ++i) dl[i] = bad ? 0.0 : F[i];
-        lu_solve(M, piv, dl);
-#pragma unroll
-        for (int i = 0; i < m; ++i) {
-            an[i] = a[i] - dl[i];
-            sc[i] = F[i] / (1.0 + fabs(a[i]));
-        }
-        const double res = rms<m>(sc);
-        growth = res > res_prev ? growth + 1 : 0;
-        res_prev = res;
-        bool conv;
-        if (cfg.mode == 1) {
-            double sn[6], ds[6];
-            stress_plain(L, e1, an, sn);
-#pragma unroll
-            for (int i = 0; i < 6; ++i) ds[i] = sn[i] - sig_prev[i];
-            const double dsig = rms<6>(ds), ref = rms<6>(sn);
-            conv = dsig <= cfg.tol * (ref > 1e-300 ? ref : 1e-300);
-#pragma unroll
-            for (int i = 0; i < 6; ++i) sig_prev[i] = sn[i];
-        } else {
-#pragma unroll
-            for (int i = 0; i < m; ++i) sc[i] = dl[i] / (1.0 + fabs(an[i]));
-            conv = rms<m>(sc) <= cfg.tol;
-        }
-#pragma unroll
-        for (int i = 0; i < m; ++i) a[i] = an[i];
-        if (bad || growth >= 5) return false;
-        if (conv) return true;
-    }
-    return false;  // iteration cap (odeint.py:400)
+struct JacShape {
+    static constexpr int m = Law::m;
+    using FT = decltype(rhs_sweep(std::declval<const Law&>(), plain_tup<6>((const double*)nullptr, seq<6>{}),
+                                  seed_tup<0>((const double*)nullptr, 1.0, seq<m>{})));
+    static constexpr uint32_t mask = tup_mask<FT>(seq<m>{});
+    // dense block = leading columns when the nonzero columns are a prefix
+    static constexpr int nd = (mask == ((1u << popc(mask)) - 1u)) ? popc(mask) : m;
+    static constexpr int nr = m - nd;
+};
+
+// f and the nd leading (structurally nonzero) columns of df/da
+template <class Law, int nd>
+AM_HD void rhs_jac_dense(const Law& L, const double* e, const double* a, double* f, double (*J)[nd]) {
+    auto fv = rhs_sweep(L, plain_tup<6>(e, seq<6>{}), seed_tup<0>(a, 1.0, seq<Law::m>{}));
+    sfor<Law::m>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        f[i] = get<i>(fv).v;
+        sfor<nd>([&](auto K) { J[i][decltype(K)::value] = get<i>(fv).template dir<decltype(K)::value>(); });
+    });
 }
 
-// ---------------------------------------------------------------- one voxel
-// _evaluate_chunk (evaluator.py:124-203) for the automatic strategy and the
-// implicit-Euler integrator.  C (if non-null) receives C[i][j].
+// ---------------------------------------------------------------- structured LU
+// Unpivoted factorisation of M = [[D, 0], [R, I]] (fast path).  It is used
+// only when it is as good as the reference's partially pivoted LU
+// (linalg.py:75-109): the multipliers must stay small (sum of |l| <= 1e3,
+// so there is no element growth that pivoting would have avoided) and every
+// pivot must be at least 1e-9 of the diagonal scale of M (far from the
+// reference's 1e-14 singularity threshold); otherwise the caller falls
+// back to the exact reference LU (cold path).  Mathematically the same
+// solve; results differ from the pivoted one by round-off only.
+template <int m, int nd>
+struct SFact {
+    static constexpr int nr = m - nd;
+    double D[nd][nd];
+    double R[nr > 0 ? nr : 1][nd];
+    double inv[nd];
+
+    // M = I - h J from the dense columns
+    AM_HD void build(const double (*J)[nd], double h) {
+#pragma unroll
+        for (int i = 0; i < nd; ++i)
+#pragma unroll
+            for (int k = 0; k < nd; ++k) D[i][k] = (i == k ? 1.0 : 0.0) - h * J[i][k];
+#pragma unroll
+        for (int r = 0; r < nr; ++r)
+#pragma unroll
+            for (int k = 0; k < nd; ++k) R[r][k] = 0.0 - h * J[nd + r][k];
+    }
+
+    AM_HD bool factor() {
+        // guard terms are sums of absolute values (DADD with |.| operand
+        // modifiers, no compare/select chains): lsum bounds every multiplier,
+        // dsum is the diagonal scale of M
+        double dsum = double(nr), lsum = 0.0;
+#pragma unroll
+        for (int k = 0; k < nd; ++k) dsum += fabs(D[k][k]);
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < nd; ++k) {
+            const double p = D[k][k];
+            ok = ok && (fabs(p) >= 1e-9 * dsum);
+            const double iv = 1.0 / p;
+            inv[k] = iv;
+#pragma unroll
+            for (int i = k + 1; i < nd; ++i) {
+                const double l = D[i][k] * iv;
+                lsum += fabs(l);
+                D[i][k] = l;
+#pragma unroll
+                for (int j = k + 1; j < nd; ++j) D[i][j] = fma(-l, D[k][j], D[i][j]);
+            }
+#pragma unroll
+            for (int r = 0; r < nr; ++r) {
+                const double l = R[r][k] * iv;
+                lsum += fabs(l);
+                R[r][k] = l;
+#pragma unroll
+                for (int j = k + 1; j < nd; ++j) R[r][j] = fma(-l, D[k][j], R[r][j]);
+            }
+        }
+        // NaN anywhere makes a comparison false; inf makes dsum or lsum inf
+        return ok && lsum <= 1e3 && dsum < INFINITY;
+    }
+
+    AM_HD void solve(double* x) const {
+#pragma unroll
+        for (int i = 1; i < nd; ++i)
+#pragma unroll
+            for (int k = 0; k < i; ++k) x[i] = fma(-D[i][k], x[k], x[i]);
+#pragma unroll
+        for (int r = 0; r < nr; ++r)
+#pragma unroll
+            for (int k = 0; k < nd; ++k) x[nd + r] = fma(-R[r][k], x[k], x[nd + r]);
+#pragma unroll
+        for (int i = nd - 1; i >= 0; --i) {
+#pragma unroll
+            for (int j = i + 1; j < nd; ++j) x[i] = fma(-D[i][j], x[j], x[i]);
+            x[i] *= inv[i];
+        }
+    }
+};
+
+// ---------------------------------------------------------------- exact (cold) path
+// The reference's dense partially pivoted LU (linalg.py:75-143) on
+// M = I - h df/da at state a, solving M x = rhs in place.  Returns the
+// reference's ok flag (all |pivot| >= 1e-14 max|M|).  Used when the fast
+// path's pivot guard trips (ill-conditioned or non-finite iteration
+// matrix) so that such voxels see exactly the reference's arithmetic;
+// `zero_rhs_if_bad` reproduces odeint.py:381-382 (solve with a zero
+// right-hand side when the factorisation or F is bad).
 template <class Law>
-AM_HD int eval_voxel(const Law& L, const NewtonCfg& cfg, const double* eps_n, const double* a_n,
-                     const double* eps_np1, double dt, double* sig, double* a_out, double (*C)[6], int& iters) {
+AM_COLD bool exact_solve(const Law& L, const double* e1, const double* a, double h, double* xp, bool zero_rhs_if_bad,
+                         bool rhs_finite) {
+    constexpr int m = Law::m;
+    double f[m], M[m][m], x[m];
+    int piv[m];
+    for (int i = 0; i < m; ++i) x[i] = xp[i];
+    rhs_jac_a(L, e1, a, f, M);
+    for (int i = 0; i < m; ++i)
+        for (int k = 0; k < m; ++k) M[i][k] = (i == k ? 1.0 : 0.0) - h * M[i][k];
+    const bool ok = lu_factor(M, piv);
+    if (zero_rhs_if_bad && (!ok || !rhs_finite))
+        for (int i = 0; i < m; ++i) x[i] = 0.0;
+    lu_solve(M, piv, x);
+    for (int i = 0; i < m; ++i) xp[i] = x[i];
+    return ok;
+}
+
+// ---------------------------------------------------------------- tangent sinks
+// Receivers of the consistent tangent C[i][j] = dsigma_i/deps_j, one
+// column j (compile-time after inlining) at a time.
+struct NoSink {
+    AM_HD void col(int, const double*) {}
+};
+template <class Sink>
+AM_HD void put_all(Sink& sink, const double (*C)[6]) {
+    sfor<6>([&](auto J) {
+        constexpr int j = decltype(J)::value;
+        double c[6];
+        for (int i = 0; i < 6; ++i) c[i] = C[i][j];
+        sink.col(j, c);
+    });
+}
+
+// strain payloads: eps_i seeded with direction i - J0 (value s) for
+// J0 <= i < J0 + NJ, plain otherwise
+template <int J0, int NJ, int I>
+AM_HD auto seed_or_plain(double v, double s) {
+    if constexpr (I >= J0 && I < J0 + NJ) return seed<I - J0>(v, s);
+    else return plain(v);
+}
+template <int J0, int NJ, int... I>
+AM_HD auto eps_seed_block(const double* e, double s, std::integer_sequence<int, I...>) {
+    return tup(seed_or_plain<J0, NJ, I>(e[I], s)...);
+}
+// state payloads (a_k, da[k][0..NJ-1]) (gsm.py:532)
+template <int NJ, int... I>
+AM_HD auto da_block_tup(const double* a, const double (*da)[NJ], std::integer_sequence<int, I...>) {
+    auto mk = [&](int k) {
+        D<(1u << NJ) - 1u> p;
+        p.v = a[k];
+        for (int j = 0; j < NJ; ++j) p.d[j] = da[k][j];
+        return p;
+    };
+    return tup(mk(I)...);
+}
+
+// Columns J0 .. J0+NJ-1 of the consistent tangent (odeint.py:417-426 then
+// gsm.py:520-551): df/deps_{n+1} for these strain directions (rhs_dual,
+// eps seeded r * e_j), (I - h J) da = 0 + h df/deps per column with the
+// factorisation of the converged iteration matrix, then the stress sweep at
+// (eps_{n+1}, clamped a) seeded (e_j, da[:, j]).  Each direction of a
+// forward dual is computed independently, so blocks of directions give the
+// same numbers as the reference's W = 6 sweeps; blocks keep the register
+// footprint of the tangent phase small.
+template <int J0, int NJ, class Law, class Fact, class Sink>
+AM_HD void tangent_block(const Law& L, const double* e1, double r, double h, const double* a, const double* ac,
+                         const double* eps_np1, const Fact& fac, bool fast, double* sig, Sink& sink) {
+    constexpr int m = Law::m;
+    auto fv = rhs_sweep(L, eps_seed_block<J0, NJ>(e1, r, seq<6>{}), plain_tup<m>(a, seq<m>{}));
+    double da[m][NJ];
+    sfor<NJ>([&](auto Jc) {
+        constexpr int jj = decltype(Jc)::value;
+        double x[m];
+        sfor<m>([&](auto I) { x[decltype(I)::value] = 0.0 + h * get<decltype(I)::value>(fv).template dir<jj>(); });
+        if (fast) fac.solve(x);
+        else exact_solve(L, e1, a, h, x, false, true);
+#pragma unroll
+        for (int i = 0; i < m; ++i) da[i][jj] = x[i];
+    });
+    auto s = stress_sweep(L, eps_seed_block<J0, NJ>(eps_np1, 1.0, seq<6>{}), da_block_tup<NJ>(ac, da, seq<m>{}));
+    sfor<NJ>([&](auto Jc) {
+        constexpr int jj = decltype(Jc)::value;
+        double c[6];
+        sfor<6>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            c[i] = get<i>(s).template dir<jj>();
+            sig[i] = get<i>(s).v;
+        });
+        sink.col(J0 + jj, c);
+    });
+}
+
+// ---------------------------------------------------------------- one point
+// _evaluate_chunk (evaluator.py:124-203) for strategy="automatic" and the
+// implicit-Euler integrator is split in two phases so that the hot Newton
+// loop and the once-per-point tangent post-process can run as separate
+// kernels with different register budgets:
+//   newton_point:  MaterialStepProblem + _newton_implicit_euler
+//                  (odeint.py:241-264, 357-401) -> unclamped state a
+//   stress_point:  clamp_state (evaluator.py:198) + stress (evaluator.py:202)
+//   tangent_point: tangent post-process (odeint.py:417-426) at the unclamped
+//                  a, clamp, stress_and_tangent (gsm.py:520-551)
+// Both phases are pure functions of the point's inputs, so the split does
+// not change any result.
+
+// MaterialStepProblem (odeint.py:241-264): t1 = 0 + h, ramp r = min(t1/dt, 1),
+// eps(t1) = eps_n + r (eps_{n+1} - eps_n)
+AM_HD double step_strain(const double* eps_n, const double* eps_np1, double dt, double* e1) {
+    const double h = dt, t1 = 0.0 + h;
+    double r = t1 / dt;
+    r = (r > 1.0) ? 1.0 : r;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) e1[i] = eps_n[i] + r * (eps_np1[i] - eps_n[i]);
+    return r;
+}
+
+// Newton of one point; returns status bits (ST_NEWTON on failure), writes the
+// unclamped state to a and the per-point Newton count (the number of
+// rhs_and_jac evaluations the reference makes for this point) to iters.
+// Mode: 0 internal / 1 stress convergence (odeint.py:388-395).
+// dt == 0 (frozen, evaluator.py:142-170): a = a_n, no iteration.
+template <class Law, int Mode>
+AM_HD int newton_point(const Law& L, const NewtonCfg& cfg, const double* eps_n, const double* a_n,
+                       const double* eps_np1, double dt, double* a, int& iters) {
     constexpr int m = Law::m;
     iters = 0;
+#pragma unroll
+    for (int i = 0; i < m; ++i) a[i] = a_n[i];
     if constexpr (m == 0) {
-        if (C) stress_tangent(L, eps_np1, a_n, nullptr, sig, C);
-        else stress_plain(L, eps_np1, a_n, sig);
         return 0;
     } else {
-        if (dt == 0.0) {  // frozen (evaluator.py:142-170): a = a_n, no clamp
+        if (dt == 0.0) return 0;
+        constexpr int nd = JacShape<Law>::nd;
+        const double h = dt;
+        double e1[6];
+        step_strain(eps_n, eps_np1, dt, e1);
+        double res_prev = INFINITY;
+        int growth = 0;
+        double sig_prev[6];
+        if constexpr (Mode == 1) stress_plain(L, e1, a, sig_prev);
+        for (;;) {
+            double f[m], J[m][nd], F[m], dl[m];
+            rhs_jac_dense<Law, nd>(L, e1, a, f, J);
+            SFact<m, nd> fac;
+            fac.build(J, h);
+            const bool fast = fac.factor();
+            ++iters;
+            bool finite = true;
 #pragma unroll
-            for (int i = 0; i < m; ++i) a_out[i] = a_n[i];
-            stress_plain(L, eps_np1, a_n, sig);
-            if (C) {
-                double s2[6];
-                stress_tangent(L, eps_np1, a_n, nullptr, s2, C);
+            for (int i = 0; i < m; ++i) {
+                F[i] = a[i] - a_n[i] - h * f[i];
+                finite = finite && (F[i] - F[i] == 0.0);  // isfinite
+                dl[i] = F[i];
             }
+            bool bad;
+            if (fast) {
+                bad = !finite;
+                if (bad) {
+#pragma unroll
+                    for (int i = 0; i < m; ++i) dl[i] = 0.0;
+                }
+                fac.solve(dl);
+            } else {
+                bad = !exact_solve(L, e1, a, h, dl, true, finite) || !finite;
+            }
+            double an[m], sc[m];
+#pragma unroll
+            for (int i = 0; i < m; ++i) {
+                an[i] = a[i] - dl[i];
+                sc[i] = F[i] / (1.0 + fabs(a[i]));
+            }
+            const double res = rms<m>(sc);
+            growth = res > res_prev ? growth + 1 : 0;
+            res_prev = res;
+            bool conv;
+            if constexpr (Mode == 1) {
+                double sn[6], ds[6];
+                stress_plain(L, e1, an, sn);
+#pragma unroll
+                for (int i = 0; i < 6; ++i) ds[i] = sn[i] - sig_prev[i];
+                const double dsig = rms<6>(ds), ref = rms<6>(sn);
+                conv = dsig <= cfg.tol * (ref > 1e-300 ? ref : 1e-300);
+#pragma unroll
+                for (int i = 0; i < 6; ++i) sig_prev[i] = sn[i];
+            } else {
+#pragma unroll
+                for (int i = 0; i < m; ++i) sc[i] = dl[i] / (1.0 + fabs(an[i]));
+                conv = rms<m>(sc) <= cfg.tol;
+            }
+#pragma unroll
+            for (int i = 0; i < m; ++i) a[i] = an[i];
+            if (bad || growth >= 5) return ST_NEWTON;  // odeint.py:397
+            if (conv) return 0;
+            if (iters >= cfg.max_it) return ST_NEWTON;  // iteration cap (odeint.py:400)
+        }
+    }
+}
+
+// clamp_state (gsm.py:252-256): alpha >= 0; identity for laws without state
+template <class Law>
+AM_HD void clamp_state(const double* a, double* ac) {
+    constexpr int m = Law::m;
+#pragma unroll
+    for (int i = 0; i < m; ++i) ac[i] = a[i];
+    if constexpr (m > 0) ac[m - 1] = ac[m - 1] < 0.0 ? 0.0 : ac[m - 1];
+}
+
+// sigma at eps_{n+1} and the clamped state (evaluator.py:198-202); writes
+// the clamped state to ac
+template <class Law>
+AM_HD void stress_point(const Law& L, const double* eps_np1, const double* a, double* ac, double* sig) {
+    clamp_state<Law>(a, ac);
+    stress_plain(L, eps_np1, ac, sig);
+}
+
+// Tangent phase for a point whose Newton converged to the unclamped state a:
+// the post-process of implicit_euler_step (odeint.py:417-426: M = I - h J at
+// a, "six additional linear system solves") and stress_and_tangent at the
+// clamped state (gsm.py:520-551).  Frozen points (dt == 0) get the elastic
+// tangent at a_n (evaluator.py:145-148), laws without state the stiffness
+// (evaluator.py:134-138).  Writes the clamped state to ac, sigma, and C to
+// the sink.  Returns ST_SINGULAR when the reference's check_singular LU
+// would raise (odeint.py:424).
+template <class Law, class Sink>
+AM_HD int tangent_point(const Law& L, const double* eps_n, const double* eps_np1, double dt, const double* a,
+                        double* ac, double* sig, Sink& sink) {
+    constexpr int m = Law::m;
+    clamp_state<Law>(a, ac);
+    if constexpr (m == 0) {
+        double C[6][6];
+        stress_tangent(L, eps_np1, a, nullptr, sig, C);
+        put_all(sink, C);
+        return 0;
+    } else {
+        if (dt == 0.0) {
+            double C[6][6], s2[6];
+            stress_plain(L, eps_np1, a, sig);
+            stress_tangent(L, eps_np1, a, nullptr, s2, C);
+            put_all(sink, C);
             return 0;
         }
-        int status = 0;
-        // MaterialStepProblem (odeint.py:241-264): t1 = 0 + h, ramp r = min(t1/dt, 1)
-        const double h = dt, t1 = 0.0 + h;
-        double r = t1 / dt;
-        r = (r > 1.0) ? 1.0 : r;
+        constexpr int nd = JacShape<Law>::nd;
+        const double h = dt;
         double e1[6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) e1[i] = eps_n[i] + r * (eps_np1[i] - eps_n[i]);
-        double a[m];
-        if (!newton_ie(L, cfg, e1, h, a_n, a, iters)) status |= ST_NEWTON;
-        double da[m][6];
-        if (C) {
-            // tangent post-process (odeint.py:417-426) at the integrated,
-            // not yet clamped, state: (I - h J) da = 0 + h df/deps
-            double J[m][m], f[m];
-            int piv[m];
-            rhs_jac_eps(L, e1, r, a, da);
-            rhs_jac_a(L, e1, a, f, J);
-#pragma unroll
-            for (int i = 0; i < m; ++i)
-#pragma unroll
-                for (int k = 0; k < m; ++k) J[i][k] = (i == k ? 1.0 : 0.0) - h * J[i][k];
-            if (!lu_factor(J, piv)) status |= ST_SINGULAR;
-#pragma unroll
-            for (int j = 0; j < 6; ++j) {
-                double x[m];
-#pragma unroll
-                for (int i = 0; i < m; ++i) x[i] = 0.0 + h * da[i][j];
-                lu_solve(J, piv, x);
-#pragma unroll
-                for (int i = 0; i < m; ++i) da[i][j] = x[i];
-            }
+        const double r = step_strain(eps_n, eps_np1, dt, e1);
+        int status = 0;
+        double f[m], J[m][nd];
+        rhs_jac_dense<Law, nd>(L, e1, a, f, J);
+        SFact<m, nd> fac;
+        fac.build(J, h);
+        const bool fast = fac.factor();
+        if (!fast) {
+            double x[m];
+            for (int i = 0; i < m; ++i) x[i] = 0.0;
+            if (!exact_solve(L, e1, a, h, x, false, true)) status |= ST_SINGULAR;
         }
-        a[6] = a[6] < 0.0 ? 0.0 : a[6];  // clamp_state (gsm.py:252-256, evaluator.py:198)
-#pragma unroll
-        for (int i = 0; i < m; ++i) a_out[i] = a[i];
-        if (C) stress_tangent(L, eps_np1, a, da, sig, C);
-        else stress_plain(L, eps_np1, a, sig);
+#ifndef AM_TAN_BLOCK
+#define AM_TAN_BLOCK 2
+#endif
+        // strain directions in blocks of AM_TAN_BLOCK columns
+        sfor<6 / AM_TAN_BLOCK>([&](auto Bk) {
+            tangent_block<decltype(Bk)::value * AM_TAN_BLOCK, AM_TAN_BLOCK>(L, e1, r, h, a, ac, eps_np1, fac, fast,
+                                                                            sig, sink);
+        });
         return status;
     }
+}
+
+// A failed point has no tangent (the reference raises NewtonDivergenceError
+// before the post-process, odeint.py:415-416): NaN columns, stress at the
+// returned state.
+template <class Law, class Sink>
+AM_HD void failed_point(const Law& L, const double* eps_np1, const double* a, double* ac, double* sig, Sink& sink) {
+    stress_point(L, eps_np1, a, ac, sig);
+    double c[6];
+    for (int i = 0; i < 6; ++i) c[i] = NAN;
+    sfor<6>([&](auto J) { sink.col(decltype(J)::value, c); });
 }
 
 }  // namespace am
