@@ -128,6 +128,74 @@ int am_eval_batch_host(const am_law *law, const am_cfg *cfg, int64_t B,
 int am_constitutive_host(const am_law *law, int64_t B, const double *eps, const double *a,
                          double *sigma, double *A, double *f, double *dfda, double *dfde);
 
+/* ---------------------------------------------------------------- basic scheme
+ * am_solver -- replaces gsmkit.homogenize.Homogenizer (homogenize.py:345-480)
+ * on one GPU: the fields, per-phase internal states, cuFFT plans and
+ * workspaces live on the device for the solver's lifetime.  A handle is
+ * single-threaded (like Homogenizer).  Host field layout is component-first
+ * (6, nx, ny, nz), C order, exactly the reference's.
+ */
+typedef struct am_solver am_solver;
+
+typedef struct am_stepinfo {       /* homogenize.StepInfo (homogenize.py:337-342) */
+    int32_t iterations;
+    int32_t converged;
+    double residual;               /* last history entry max(res, res_bc) */
+    double mean_substeps;
+    double ebar[6];                /* mean strain of the returned (last evaluated) field */
+    double sig_bar[6];             /* mean stress of the returned field */
+} am_stepinfo;
+
+enum { AM_FIELD_EPS = 0, AM_FIELD_EPS_N = 1, AM_FIELD_SIGMA = 2 };
+
+/* Homogenizer.__init__ minus the reference (set with am_solver_set_reference):
+ * ids (nx*ny*nz uint8, C order) index `laws`; state starts at zero
+ * (VoxelGrid, homogenize.py:85-99). */
+int am_solver_create(int nx, int ny, int nz, const uint8_t *ids, int nmat, const am_law *laws,
+                     const am_cfg *cfg, am_solver **out);
+int am_solver_destroy(am_solver *h);
+/* Homogenizer.set_reference / .reference (homogenize.py:378-380) */
+int am_solver_set_reference(am_solver *h, double lam, double mu);
+int am_solver_get_reference(am_solver *h, double *lam, double *mu);
+/* Homogenizer.ebar_n (homogenize.py:355) */
+int am_solver_set_mean(am_solver *h, const double *ebar_n);
+/* Homogenizer.solve_step (homogenize.py:425-472): converges the basic
+ * scheme for one loading step; `history` (optional, history_cap entries)
+ * receives max(res, res_bc) per iteration.  AM_ERR_NOT_CONVERGED after
+ * max_iterations (SolverError), AM_ERR_NEWTON if a voxel's Newton failed.
+ * The converged fields stay on the device (am_solver_get_field). */
+int am_solver_solve_step(am_solver *h, const double *ebar_target, double dt, const uint8_t *free_mask,
+                         double tol, int max_iterations, am_stepinfo *info, double *history, int history_cap);
+/* Homogenizer.commit_step (homogenize.py:474-480) for the solver's eps */
+int am_solver_commit(am_solver *h, const double *ebar);
+/* Homogenizer.evaluate_field (homogenize.py:389-421) of the device eps,
+ * without tangent: sigma field and pending states */
+int am_solver_evaluate(am_solver *h, double dt);
+/* evaluate_field(want_tangent=True) fused with reference_update
+ * (homogenize.py:509-513): Cbar (36, optional) = voxel mean of C,
+ * lam_mu (2, optional) = reference_update(C field); C_out (optional, host
+ * (N, 6, 6)) receives the tangent field itself. */
+int am_solver_tangent_sweep(am_solver *h, double dt, double *Cbar, double *lam_mu, double *C_out);
+int am_solver_get_field(am_solver *h, int which, double *out);
+int am_solver_set_field(am_solver *h, int which, const double *in);
+/* per-phase internal state, host (count, m); pending = 1 for the state of
+ * the last evaluation, 0 for the committed one (VoxelGrid.state) */
+int am_solver_get_state(am_solver *h, int phase, int pending, double *out);
+int am_solver_set_state(am_solver *h, int phase, const double *in);
+int am_solver_phase_count(am_solver *h, int phase, int64_t *count);
+int am_solver_synchronize(am_solver *h);
+int am_solver_stream(am_solver *h, void **stream);
+
+/* ---------------------------------------------------------------- field operators (host arrays) */
+/* GreenOperator(dims, ReferenceMaterial(lam, mu)).apply(tau) (homogenize.py:174-233) */
+int am_green_apply_host(int nx, int ny, int nz, double lam, double mu, const double *tau, double *out);
+/* equilibrium_residual(sig) (homogenize.py:241-267) */
+int am_equilibrium_residual_host(int nx, int ny, int nz, const double *sig, double *res);
+/* apply_isotropic(ref, eps) (homogenize.py:270-281), fields (6, N) */
+int am_apply_isotropic_host(int64_t N, double lam, double mu, const double *eps, double *out);
+/* reference_update(C_field) (homogenize.py:307-329), C (n, 6, 6) */
+int am_reference_update_host(int64_t n, const double *C, double *lam, double *mu);
+
 /* ---------------------------------------------------------------- diagnostics
  * am_probe_fp64_tflops -- sustained fp64 FMA throughput of the current
  * device (the roofline denominator of the material kernel; no reference

@@ -56,6 +56,7 @@ class am_stepinfo(ctypes.Structure):
     _fields_ = [
         ("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
         ("residual", ctypes.c_double), ("mean_substeps", ctypes.c_double),
+        ("ebar", ctypes.c_double * 6), ("sig_bar", ctypes.c_double * 6),
     ]
 
 
@@ -86,6 +87,34 @@ SIGNATURES = {
     "am_constitutive_host": (ctypes.c_int, [
         ctypes.POINTER(am_law), ctypes.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
     ]),
+    # basic scheme (solver.cu)
+    "am_solver_create": (ctypes.c_int, [
+        ctypes.c_int, ctypes.c_int, ctypes.c_int, _u8p, ctypes.c_int, ctypes.POINTER(am_law), ctypes.POINTER(am_cfg),
+        ctypes.POINTER(_vp),
+    ]),
+    "am_solver_destroy": (ctypes.c_int, [_vp]),
+    "am_solver_set_reference": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_double]),
+    "am_solver_get_reference": (ctypes.c_int, [_vp, _dp, _dp]),
+    "am_solver_set_mean": (ctypes.c_int, [_vp, _dp]),
+    "am_solver_solve_step": (ctypes.c_int, [
+        _vp, _dp, ctypes.c_double, _u8p, ctypes.c_double, ctypes.c_int, ctypes.POINTER(am_stepinfo), _dp, ctypes.c_int,
+    ]),
+    "am_solver_commit": (ctypes.c_int, [_vp, _dp]),
+    "am_solver_evaluate": (ctypes.c_int, [_vp, ctypes.c_double]),
+    "am_solver_tangent_sweep": (ctypes.c_int, [_vp, ctypes.c_double, _dp, _dp, _dp]),
+    "am_solver_get_field": (ctypes.c_int, [_vp, ctypes.c_int, _dp]),
+    "am_solver_set_field": (ctypes.c_int, [_vp, ctypes.c_int, _dp]),
+    "am_solver_get_state": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _dp]),
+    "am_solver_set_state": (ctypes.c_int, [_vp, ctypes.c_int, _dp]),
+    "am_solver_phase_count": (ctypes.c_int, [_vp, ctypes.c_int, _i64p]),
+    "am_solver_synchronize": (ctypes.c_int, [_vp]),
+    "am_solver_stream": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
+    "am_green_apply_host": (ctypes.c_int, [
+        ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, _dp, _dp,
+    ]),
+    "am_equilibrium_residual_host": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _dp]),
+    "am_apply_isotropic_host": (ctypes.c_int, [ctypes.c_int64, ctypes.c_double, ctypes.c_double, _dp, _dp]),
+    "am_reference_update_host": (ctypes.c_int, [ctypes.c_int64, _dp, _dp, _dp]),
 }
 
 _LIB = None
@@ -178,6 +207,10 @@ def check(rc, where=""):
         raise NewtonDivergenceError(msg)
     if rc == AM_ERR_SINGULAR:
         raise SingularMatrixError(msg)
+    if rc == AM_ERR_NOT_CONVERGED:
+        from .homogenize import SolverError
+
+        raise SolverError(msg)
     if rc in (AM_ERR_ARG, AM_ERR_NONFINITE):
         raise ValueError(msg)
     raise RuntimeError(f"libautomat error {rc}: {msg}")

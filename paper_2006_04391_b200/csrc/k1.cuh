@@ -1,0 +1,46 @@
+// k1.cuh -- launch interface of the material kernel (K1) shared by the
+// material-point entry points (material.cu) and the basic-scheme solver
+// (solver.cu).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "../../include/automat.h"
+#include "newton_cfg.cuh"
+
+namespace am {
+
+struct Layout {
+    int64_t cs, es;  // element (c, b) at p[c * cs + b * es]
+};
+
+struct KArgs {
+    int64_t B;
+    const int64_t* gidx;  // optional gather/scatter index for eps_n / eps_np1 / sigma
+    const double* eps_n;
+    const double* a_n;
+    const double* eps_np1;
+    const double* dt;
+    double dt_scalar;
+    Layout le, la, lc;
+    double* sigma;
+    double* a_out;
+    double* C;
+    int32_t* iters;
+    uint8_t* status;
+    uint32_t* flags;
+    NewtonCfg ncfg;
+};
+
+// validation and dispatch (material.cu)
+int check_law(const am_law* law);
+int check_cfg(const am_cfg* cfg);
+int law_m(const am_law* law);
+NewtonCfg newton_cfg(const am_cfg* cfg);
+// enqueue K1 on stream s: Newton (+ clamp + stress), or with k.C the Newton
+// then tangent kernels; per-point status bits OR-ed into *k.flags
+int launch_material(const am_law* law, const KArgs& k, cudaStream_t s);
+
+}  // namespace am

@@ -15,31 +15,10 @@
 #include <vector>
 
 #include "common.cuh"
+#include "k1.cuh"
 #include "material.cuh"
 
 namespace am {
-
-struct Layout {
-    int64_t cs, es;  // element (c, b) at p[c * cs + b * es]
-};
-
-struct KArgs {
-    int64_t B;
-    const int64_t* gidx;  // optional gather/scatter index for eps_n / eps_np1 / sigma
-    const double* eps_n;
-    const double* a_n;
-    const double* eps_np1;
-    const double* dt;
-    double dt_scalar;
-    Layout le, la, lc;
-    double* sigma;
-    double* a_out;
-    double* C;
-    int32_t* iters;
-    uint8_t* status;
-    uint32_t* flags;
-    NewtonCfg ncfg;
-};
 
 // writes C[i][j] of item `off` to C[(i * 6 + j) * cs + off]
 struct GlobalSink {
@@ -187,7 +166,7 @@ __global__ void k_constitutive(Law L, int64_t B, const double* eps, const double
     }
 }
 
-static int check_law(const am_law* law) {
+int check_law(const am_law* law) {
     if (!law) return fail(AM_ERR_ARG, "law is NULL");
     if (law->kind != AM_LAW_LINEAR_ELASTIC && law->kind != AM_LAW_MICHEL_SUQUET)
         return fail(AM_ERR_CONFIG, "unknown law kind %d (only LinearElastic and MichelSuquet have device potentials)",
@@ -195,7 +174,7 @@ static int check_law(const am_law* law) {
     return AM_OK;
 }
 
-static int check_cfg(const am_cfg* cfg) {
+int check_cfg(const am_cfg* cfg) {
     if (!cfg) return fail(AM_ERR_ARG, "cfg is NULL");
     if (cfg->strategy != AM_STRATEGY_AUTOMATIC || cfg->integrator != AM_INTEGRATOR_IMPLICIT_EULER)
         return fail(AM_ERR_CONFIG,
@@ -208,7 +187,7 @@ static int check_cfg(const am_cfg* cfg) {
     return AM_OK;
 }
 
-static NewtonCfg newton_cfg(const am_cfg* cfg) { return NewtonCfg{cfg->newton_mode, cfg->max_newton, cfg->newton_tol}; }
+NewtonCfg newton_cfg(const am_cfg* cfg) { return NewtonCfg{cfg->newton_mode, cfg->max_newton, cfg->newton_tol}; }
 
 template <class Law>
 static int launch_law(const Law& L, KArgs k, cudaStream_t s) {
@@ -244,7 +223,7 @@ static int launch_law(const Law& L, KArgs k, cudaStream_t s) {
     return AM_OK;
 }
 
-static int launch(const am_law* law, const KArgs& k, cudaStream_t s) {
+int launch_material(const am_law* law, const KArgs& k, cudaStream_t s) {
     if (k.B == 0) return AM_OK;
     if (law->kind == AM_LAW_MICHEL_SUQUET)
         return launch_law(
@@ -253,22 +232,6 @@ static int launch(const am_law* law, const KArgs& k, cudaStream_t s) {
 }
 
 int law_m(const am_law* law) { return law->kind == AM_LAW_MICHEL_SUQUET ? 7 : 0; }
-
-// internal entry used by the basic-scheme solver: gathers eps fields through
-// gidx, per-material state arrays are SoA with stride Bm.
-int eval_gather(const am_law* law, const am_cfg* cfg, int64_t B, const int64_t* gidx, int64_t N,
-                const double* eps_n, const double* a_n, const double* eps_np1, double dt, int want_tangent,
-                double* sigma, double* a_out, double* C, int32_t* iters, uint8_t* status, uint32_t* flags,
-                cudaStream_t s) {
-    KArgs k{};
-    k.B = B; k.gidx = gidx;
-    k.eps_n = eps_n; k.a_n = a_n; k.eps_np1 = eps_np1; k.dt = nullptr; k.dt_scalar = dt;
-    k.le = {N, 1}; k.la = {B, 1}; k.lc = {B, 1};
-    k.sigma = sigma; k.a_out = a_out; k.C = want_tangent ? C : nullptr;
-    k.iters = iters; k.status = status; k.flags = flags;
-    k.ncfg = newton_cfg(cfg);
-    return launch(law, k, s);
-}
 
 }  // namespace am
 
@@ -291,7 +254,7 @@ extern "C" int am_eval_batch(const am_law* law, const am_cfg* cfg, int64_t B, co
     k.sigma = sigma; k.a_out = a_out; k.C = want_tangent ? C : nullptr;
     k.iters = newton_iters; k.status = status; k.flags = flags;
     k.ncfg = newton_cfg(cfg);
-    return launch(law, k, (cudaStream_t)stream);
+    return launch_material(law, k, (cudaStream_t)stream);
 }
 
 namespace {
@@ -388,7 +351,7 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
         k.sigma = d_sig; k.a_out = d_ao; k.C = want_tangent ? d_C : nullptr;
         k.iters = P.iters[s]; k.status = P.status[s]; k.flags = P.flags + s;
         k.ncfg = newton_cfg(cfg);
-        AM_TRY(launch(law, k, st));
+        AM_TRY(launch_material(law, k, st));
         AM_CUDA(cudaMemcpyAsync(sigma + 6 * lo, d_sig, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, st));
         if (m) AM_CUDA(cudaMemcpyAsync(a_out + m * lo, d_ao, sizeof(double) * m * n, cudaMemcpyDeviceToHost, st));
         if (want_tangent)

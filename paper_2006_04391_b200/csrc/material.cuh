@@ -18,6 +18,8 @@
 #include "ad.cuh"
 #include "laws.cuh"
 
+#include "newton_cfg.cuh"
+
 namespace am {
 
 template <int N>
@@ -25,11 +27,6 @@ using seq = std::make_integer_sequence<int, N>;
 
 enum : int { ST_NEWTON = 1, ST_SINGULAR = 2, ST_NONFINITE = 4 };
 
-struct NewtonCfg {
-    int mode;      // 0 internal (RMS of the applied step), 1 stress
-    int max_it;    // odeint.py:371
-    double tol;    // implicit_euler_step newton_tol (odeint.py:404)
-};
 
 // ---------------------------------------------------------------- tuple helpers
 template <int N, int... I>
