@@ -29,7 +29,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "voxel stress+tangent evals/sec (fp64)"
+METRIC = "voxel stress+tangent evals/sec (fp64) and basic-scheme iterations/sec at 256³"
 UNIT = "evals/s"
 B_DEFAULT = 1 << 20
 
@@ -156,6 +156,68 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def basic_scheme(n, lib, dev):
+    """Basic-scheme iterations/s on config 4's microstructure (toy_mmc_grid(n),
+    elasto-viscoplastic matrix + elastic fibre), load step 1 of
+    LoadingPath(steps=20) with mixed BCs, device-resident; per-phase times
+    from am_solver_timing (CUDA events on the solver stream)."""
+    import torch
+
+    from paper_2006_04391_b200 import _lib, homogenize as H
+    from paper_2006_04391_b200.evaluator import StrategyConfig
+
+    cfg = StrategyConfig(strategy="automatic", integrator="implicit-euler")
+    grid = H.toy_mmc_grid(n)
+    hom = H.Homogenizer(grid, cfg)
+    sp = ctypes.c_void_p()
+    _lib.check(lib.am_solver_stream(hom._h, ctypes.byref(sp)))
+    stream = torch.cuda.ExternalStream(sp.value, device=dev)
+    path = H.LoadingPath(steps=20)
+    times = path.times()
+    target = np.zeros(6)
+    target[0] = path.eps_xx(times)[1]
+    free = np.array([False, True, True, True, True, True])
+    _lib.check(lib.am_solver_timing(hom._h, 1, None))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with Clocks(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        info, _ = hom._solve(target, times[1] - times[0], free)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ph = np.zeros(5)
+    _lib.check(lib.am_solver_timing(hom._h, -1, _lib.ptr(ph)))
+    iters = info.iterations
+    N = n ** 3
+    Nh = n * n * (n // 2 + 1)
+    it_t = ph[4] or 1.0
+    fourier_ms = ph[2] / it_t
+    fourier_bytes = 4 * 96.0 * Nh  # read shat, ehat; write ehat, shat (complex128 x 6)
+    return {
+        "metric": "basic-scheme iterations/s", "value": iters / (ms * 1e-3), "unit": "it/s",
+        "config": {"workload": f"config 4 grid toy_mmc_grid({n}) (EVP matrix, VF 0.10 elastic fibre), "
+                               "load step 1 of LoadingPath(steps=20), mixed BC, tol 1e-5, 1 GPU",
+                   "voxels": N, "evp_voxels": int(len(grid.voxel_index[0]))},
+        "iterations": iters, "ms_total": ms, "ms_per_iteration": ms / iters,
+        "phase_ms_per_iteration": {"material": ph[0] / it_t, "d2z": ph[1] / it_t, "fourier+reduce": fourier_ms,
+                                   "origin+z2d": ph[3] / max(it_t - 1, 1)},
+        "fourier_roofline": {"bound": "hbm", "achieved": fourier_bytes / (fourier_ms * 1e-3) / 1e9,
+                             "peak": hbm_peak(), "unit": "GB/s",
+                             "frac": fourier_bytes / (fourier_ms * 1e-3) / 1e9 / hbm_peak(),
+                             "traffic_per_launch_algorithmic": fourier_bytes,
+                             "note": "k_fourier incl. the fixed-order reduction and the 64-byte D2H of the residual"},
+        "clocks": clk.summary(),
+    }
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6650.0  # B200_PROFILING.md fallback
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -164,6 +226,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=B_DEFAULT)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--basic", type=int, default=256, help="grid size n of the basic-scheme line (0: skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -206,13 +269,14 @@ def main():
     d_C = torch.empty((36, B), dtype=torch.float64, device=dev)
     d_it = torch.empty(B, dtype=torch.int32, device=dev)
     d_fl = torch.zeros(1, dtype=torch.int32, device=dev)
+    d_st = torch.empty(B, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = ctypes.c_void_p(stream.cuda_stream)
 
     def step():
         rc = lib.am_eval_batch(s_law, s_cfg, B, d_en.data_ptr(), d_an.data_ptr(), d_ep.data_ptr(), d_dt.data_ptr(),
-                               0.0, 1, d_sig.data_ptr(), d_a.data_ptr(), d_C.data_ptr(), d_it.data_ptr(), None,
-                               d_fl.data_ptr(), sp)
+                               0.0, 1, d_sig.data_ptr(), d_a.data_ptr(), d_C.data_ptr(), d_it.data_ptr(),
+                               d_st.data_ptr(), d_fl.data_ptr(), sp)
         if rc:
             _lib.check(rc)
 
@@ -295,12 +359,16 @@ def main():
                      "frac": achieved / peak.value if peak.value else None, "traffic": None,
                      "peak_source": "measured: am_probe_fp64_tflops DFMA microbenchmark on this GPU "
                                     "(MEASURED_PEAKS.json has no fp64 entry)",
-                     "work_per_launch": f"{fl:.4g} algorithmic fp64 flops (SURVEY §8d: 1072*N_it + 2273 per eval)"},
+                     "work_per_launch": f"{fl:.4g} algorithmic fp64 flops per step (SURVEY §8d: 1072*N_it + 2273 per eval); "
+                                    "one step = the Newton kernel + the tangent kernel"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "am_eval_batch_host (C ABI), pinned host AoS buffers, 2-stream chunked H2D|kernel|D2H"},
-        "gpu_launches": args.steps,
+        "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
     }
+    if args.basic:
+        line["basic_scheme"] = basic_scheme(args.basic, lib, dev)
+        line["gpu_launches_note"] = "gpu_launches counts the config-2 K1 launches of the timed region"
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)

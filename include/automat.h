@@ -184,6 +184,10 @@ int am_solver_get_state(am_solver *h, int phase, int pending, double *out);
 int am_solver_set_state(am_solver *h, int phase, const double *in);
 int am_solver_phase_count(am_solver *h, int phase, int64_t *count);
 int am_solver_synchronize(am_solver *h);
+/* per-phase device time of solve_step iterations: out[0..4] = ms in the
+ * material sweeps, D2Z, Fourier kernel + reduction, origin + Z2D, and the
+ * iteration count; enable 1 = on (reset), 0 = off, -1 = query */
+int am_solver_timing(am_solver *h, int enable, double *out);
 int am_solver_stream(am_solver *h, void **stream);
 
 /* ---------------------------------------------------------------- field operators (host arrays) */

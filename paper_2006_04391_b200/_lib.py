@@ -108,6 +108,7 @@ SIGNATURES = {
     "am_solver_set_state": (ctypes.c_int, [_vp, ctypes.c_int, _dp]),
     "am_solver_phase_count": (ctypes.c_int, [_vp, ctypes.c_int, _i64p]),
     "am_solver_synchronize": (ctypes.c_int, [_vp]),
+    "am_solver_timing": (ctypes.c_int, [_vp, ctypes.c_int, _dp]),
     "am_solver_stream": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     "am_green_apply_host": (ctypes.c_int, [
         ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, _dp, _dp,

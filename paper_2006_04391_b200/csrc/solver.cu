@@ -350,6 +350,10 @@ struct am_solver {
     double ebar[6] = {0, 0, 0, 0, 0, 0};  // mean strain of the current iterate
     bool pending = false;
     am::DevBasis db = am::DevBasis::make();
+    // optional per-phase device timing of solve_step (am_solver_timing)
+    bool timing = false;
+    cudaEvent_t ev[6] = {};
+    double t_ms[5] = {0, 0, 0, 0, 0};  // material, d2z, fourier+reduce, z2d+origin, iterations
 };
 
 namespace am {
@@ -366,6 +370,8 @@ static int solver_free(am_solver* h) {
     cudaFree(h->shat); cudaFree(h->ehat);
     cudaFree(h->partial); cudaFree(h->dsmall); cudaFreeHost(h->hsmall); cudaFree(h->flags);
     cudaFree(h->Cbuf); cudaFree(h->status); cudaFree(h->stats); cudaFreeHost(h->hstats);
+    for (auto& e : h->ev)
+        if (e) cudaEventDestroy(e);
     if (h->r2c) cufftDestroy(h->r2c);
     if (h->c2r) cufftDestroy(h->c2r);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -555,11 +561,32 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
     info->residual = 0.0;
     info->mean_substeps = 1.0;  // implicit Euler: one substep per voxel (evaluator.py:130)
     const double Nd = (double)d.N;
+    auto mark = [&](int i) -> int {
+        if (h->timing) AM_CUDA(cudaEventRecord(h->ev[i], h->stream));
+        return AM_OK;
+    };
+    auto acc = [&](int a, int b, int slot) -> int {
+        float ms = 0.f;
+        AM_CUDA(cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]));
+        h->t_ms[slot] += ms;
+        return AM_OK;
+    };
     for (int it = 1; it <= max_iterations; ++it) {
+        AM_TRY(mark(0));
         AM_TRY(material_sweep(h, dt));
+        AM_TRY(mark(1));
         AM_TRY(fft_forward(h, h->sigma, h->shat));
+        AM_TRY(mark(2));
         double o[8];
-        AM_TRY(fourier_pass(h, true, o));
+        AM_TRY(fourier_pass(h, true, o));  // synchronises the stream
+        if (h->timing) {
+            AM_CUDA(cudaEventRecord(h->ev[3], h->stream));
+            AM_CUDA(cudaEventSynchronize(h->ev[3]));
+            AM_TRY(acc(0, 1, 0));
+            AM_TRY(acc(1, 2, 1));
+            AM_TRY(acc(2, 3, 2));
+            h->t_ms[4] += 1.0;
+        }
         if ((uint32_t)o[7] & AM_VOXEL_NEWTON_FAILED) {
             info->iterations = it;
             return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel (iteration %d)", it);
@@ -598,9 +625,15 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
         }
         Vec6 eb;
         for (int i = 0; i < 6; ++i) eb.v[i] = ebar[i];
+        AM_TRY(mark(4));
         k_origin<<<1, 32, 0, h->stream>>>(h->shat, h->ehat, d.Nh, eb, Nd);
         AM_CUDA(cudaGetLastError());
         AM_TRY(fft_inverse(h, h->shat, h->eps));
+        if (h->timing) {
+            AM_TRY(mark(5));
+            AM_CUDA(cudaEventSynchronize(h->ev[5]));
+            AM_TRY(acc(4, 5, 3));
+        }
     }
     std::memcpy(h->ebar, ebar, sizeof(ebar));
     return fail(AM_ERR_NOT_CONVERGED, "basic scheme did not converge in %d iterations (last residual %.3e)",
@@ -752,6 +785,24 @@ extern "C" int am_solver_set_state(am_solver* h, int phase, const double* in) {
 extern "C" int am_solver_phase_count(am_solver* h, int phase, int64_t* count) {
     if (!h || phase < 0 || phase >= (int)h->phases.size()) return fail(AM_ERR_ARG, "bad phase");
     *count = h->phases[phase].count;
+    return AM_OK;
+}
+
+// Per-phase device time of solve_step iterations (CUDA events on the solver
+// stream): out[0..4] = ms in material sweeps, D2Z, Fourier kernel +
+// reduction, origin + Z2D, and the number of iterations timed.  enable:
+// 1 on (resets the accumulators), 0 off, -1 query only.
+extern "C" int am_solver_timing(am_solver* h, int enable, double* out) {
+    if (!h) return fail(AM_ERR_ARG, "null solver");
+    AM_CUDA(cudaSetDevice(h->device));
+    if (enable >= 0) {
+        if (enable && !h->ev[0])
+            for (auto& e : h->ev) AM_CUDA(cudaEventCreate(&e));
+        h->timing = enable != 0;
+        for (double& t : h->t_ms) t = 0.0;
+    }
+    if (out)
+        for (int i = 0; i < 5; ++i) out[i] = h->t_ms[i];
     return AM_OK;
 }
 

@@ -49,7 +49,8 @@ def summarise(path):
             v = d[key].replace(",", "")
             try:
                 if key == "gpu__time_duration.sum":
-                    x = float(v) * UNIT_SCALE.get(u.get(key, ""), 1) / 1e3  # ns -> us
+                    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+                    x = float(v) * scale.get(u.get(key, ""), 1.0)  # -> us
                 else:
                     x = float(v) * UNIT_SCALE.get(u.get(key, ""), 1)
                 v = f"{x:.6g}"
