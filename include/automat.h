@@ -153,6 +153,22 @@ enum { AM_FIELD_EPS = 0, AM_FIELD_EPS_N = 1, AM_FIELD_SIGMA = 2 };
  * (VoxelGrid, homogenize.py:85-99). */
 int am_solver_create(int nx, int ny, int nz, const uint8_t *ids, int nmat, const am_law *laws,
                      const am_cfg *cfg, am_solver **out);
+/* The same solver over nslabs x-slabs driven from this process on the
+ * current device (the distributed algorithm -- 2-D FFTs, all-to-all
+ * transposes, 1-D FFTs over x -- with device copies as the transport; used to
+ * test the multi-GPU code path on one GPU).  nslabs must divide nx and ny. */
+int am_solver_create_slabs(int nx, int ny, int nz, const uint8_t *ids, int nmat, const am_law *laws,
+                           const am_cfg *cfg, int nslabs, am_solver **out);
+/* One x-slab per process (rank of nranks) on the current device, transposes
+ * and reductions over an NCCL communicator (NVLink / NVSwitch).  `id128` is
+ * an ncclUniqueId from am_nccl_unique_id on rank 0, broadcast by the caller.
+ * Every rank passes the full ids array.  Host fields / states of this
+ * handle are the rank's slab (6, nx/nranks, ny, nz). */
+int am_nccl_unique_id(void *id128);
+int am_solver_create_nccl(int nx, int ny, int nz, const uint8_t *ids, int nmat, const am_law *laws,
+                          const am_cfg *cfg, const void *id128, int rank, int nranks, am_solver **out);
+/* slab decomposition of a handle: global slab count, first local slab, local slabs */
+int am_solver_layout(am_solver *h, int *nslabs, int *first, int *nlocal);
 int am_solver_destroy(am_solver *h);
 /* Homogenizer.set_reference / .reference (homogenize.py:378-380) */
 int am_solver_set_reference(am_solver *h, double lam, double mu);
@@ -176,6 +192,8 @@ int am_solver_evaluate(am_solver *h, double dt);
  * lam_mu (2, optional) = reference_update(C field); C_out (optional, host
  * (N, 6, 6)) receives the tangent field itself. */
 int am_solver_tangent_sweep(am_solver *h, double dt, double *Cbar, double *lam_mu, double *C_out);
+/* host (6, nx_local, ny, nz): the whole grid for handles from
+ * am_solver_create[_slabs], the rank's slab for am_solver_create_nccl */
 int am_solver_get_field(am_solver *h, int which, double *out);
 int am_solver_set_field(am_solver *h, int which, const double *in);
 /* per-phase internal state, host (count, m); pending = 1 for the state of

@@ -92,6 +92,17 @@ SIGNATURES = {
         ctypes.c_int, ctypes.c_int, ctypes.c_int, _u8p, ctypes.c_int, ctypes.POINTER(am_law), ctypes.POINTER(am_cfg),
         ctypes.POINTER(_vp),
     ]),
+    "am_solver_create_slabs": (ctypes.c_int, [
+        ctypes.c_int, ctypes.c_int, ctypes.c_int, _u8p, ctypes.c_int, ctypes.POINTER(am_law), ctypes.POINTER(am_cfg),
+        ctypes.c_int, ctypes.POINTER(_vp),
+    ]),
+    "am_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+    "am_solver_create_nccl": (ctypes.c_int, [
+        ctypes.c_int, ctypes.c_int, ctypes.c_int, _u8p, ctypes.c_int, ctypes.POINTER(am_law), ctypes.POINTER(am_cfg),
+        ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp),
+    ]),
+    "am_solver_layout": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(ctypes.c_int)]),
     "am_solver_destroy": (ctypes.c_int, [_vp]),
     "am_solver_set_reference": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_double]),
     "am_solver_get_reference": (ctypes.c_int, [_vp, _dp, _dp]),

@@ -1,33 +1,40 @@
-// solver.cu -- the Moulinec-Suquet basic scheme on one GPU (gsmkit
-// homogenize.py: Homogenizer, GreenOperator, equilibrium_residual,
-// reference_update, apply_isotropic) and its C-ABI (am_solver_*, am_*_host).
+// solver.cu -- the Moulinec-Suquet basic scheme (gsmkit homogenize.py:
+// Homogenizer, GreenOperator, equilibrium_residual, reference_update,
+// apply_isotropic) on one or more GPUs, and its C-ABI (am_solver_*,
+// am_*_host).
 //
-// Device-resident state (component-major SoA, fp64):
-//   eps, eps_n, sigma   (6, N)           strain iterate, committed strain, stress
-//   ehat                (6, N^)  cplx    rfft of eps (unnormalised), carried across iterations
-//   shat                (6, N^)  cplx    rfft of sigma, then the Z2D input of the update
-//   per phase: gidx (Bm) i64, a_n and a_pending (m, Bm)
-// with N = nx ny nz, N^ = nx ny (nz/2+1).
+// The grid is decomposed into x-slabs ("ranks").  A solver handle drives
+// either
+//   * all slabs of the grid from one process on the current device (local
+//     mode: nslabs = 1 is the plain single-GPU solver; nslabs > 1 runs the
+//     distributed algorithm with device-to-device copies as the transport,
+//     which is how the slab code is tested on a single B200), or
+//   * exactly one slab per process with an NCCL communicator over
+//     NVLink / NVSwitch (nccl mode, one process per GPU).
+//
+// Device-resident state per slab (component-major SoA, fp64):
+//   eps, eps_n, sigma (6, nxl, ny, nz)   strain iterate, committed strain, stress
+//   S, ehat                             spectra of sigma / of eps (complex128)
+//   per phase: slab-local gather index, committed + pending internal states
+// Spectral layout: one slab: cuFFT's (6, nx, ny, nz/2+1); several slabs:
+// ky-slabs [kx][c][ky_local][kz], the layout the x-transposes produce.
 //
 // One basic-scheme iteration (homogenize.py:445-465):
-//   K1   sigma = material(eps_n, a_n, eps)           per phase, gathered by gidx
-//   D2Z  shat = rfft(sigma)                          6 batched 3-D transforms
-//   K2   residual partials and, for every bin but 0, the update
-//        ehat' = -Gamma0 (shat - C0 ehat)          (= rfft of the new fluctuation)
-//        written to ehat and, scaled by 1/N, to shat (Z2D input)
-//   red  fixed-order sum of the partials; sigma_bar = shat(0)/N; D2H of 8 doubles
-//   host convergence test (strict <, homogenize.py:454), mixed-BC update of ebar
-//   bin0 ehat(0) = N ebar; Z2D eps = irfft(shat)
+//   K1    sigma = material(eps_n, a_n, eps) per phase (gathered)
+//   FFT   S = rfft(sigma)   3-D D2Z, or 2-D D2Z + pack + all-to-all + 1-D FFT(x)
+//   K2    residual partials per (ky plane, part) and, for every bin but 0,
+//         ehat' = -Gamma0 (S - C0 ehat) -> ehat, ehat'/N -> S
+//   red   fixed-order partials (independent of the slab count) -> host
+//   host  strict convergence test, mixed-BC solve (homogenize.py:454-464)
+//   bin0  ehat(0) = N ebar;  eps = irfft(S)  (inverse of FFT above)
 // Carrying ehat replaces the reference's FFT of tau = sigma - C0:eps
-// (6 forward + 6 inverse transforms per iteration instead of 12 + 6): the
-// reference's tau_hat is rfft(sigma) - C0 rfft(eps), and rfft(eps) is the
-// previous update plus the mean.
+// (6 forward + 6 inverse transforms per iteration instead of 12 + 6).
 #include <cufft.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstring>
-#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -44,17 +51,44 @@ namespace am {
         if (_r != CUFFT_SUCCESS) return ::am::fail(AM_ERR_CUDA, "%s:%d %s: cufft error %d", \
                                                    __FILE__, __LINE__, #expr, (int)_r);     \
     } while (0)
+#define AM_NCCL(expr)                                                                        \
+    do {                                                                                     \
+        ncclResult_t _r = (expr);                                                            \
+        if (_r != ncclSuccess) return ::am::fail(AM_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, \
+                                                 #expr, ncclGetErrorString(_r));             \
+    } while (0)
 
 struct Vec6 {
     double v[6];
 };
 
 constexpr int kRedThreads = 256;
-constexpr int kRedBlocks = 148 * 4;  // fixed: the reduction order never depends on the launch
+constexpr int kParts = 8;            // blocks per ky plane in the residual: fixed, so the
+                                     // reduction order never depends on the slab count
+constexpr int kRedBlocks = 148 * 4;  // k_refstats / standalone reductions
+
+// ---------------------------------------------------------------- layouts
+// spectral layout of one slab; bin (kx, ky_local, kz) of component c lives
+// at c * cs + kx * xs + kyl * nzh + kz
+struct Spec {
+    int nx, ny, nz, nzh;
+    int y0, nyl;
+    int64_t cs, xs;
+    int64_t N;  // global voxel count (normalisation)
+};
+
+static Spec spec_single(int nx, int ny, int nz) {
+    const int nzh = nz / 2 + 1;
+    return Spec{nx, ny, nz, nzh, 0, ny, (int64_t)nx * ny * nzh, (int64_t)ny * nzh, (int64_t)nx * ny * nz};
+}
+static Spec spec_slab(int nx, int ny, int nz, int y0, int nyl) {
+    const int nzh = nz / 2 + 1;
+    return Spec{nx, ny, nz, nzh, y0, nyl, (int64_t)nyl * nzh, (int64_t)6 * nyl * nzh, (int64_t)nx * ny * nz};
+}
 
 // ---------------------------------------------------------------- kernels
 __device__ __forceinline__ double block_sum(double v, double* sh) {
-    // deterministic tree: warp shuffle then the warps' partials in order
+    // deterministic: warp shuffle tree, then the warps' partials in order
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -67,49 +101,43 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return s;
 }
 
-// eps = eps_n + d (start of a loading step, homogenize.py:439)
-__global__ void k_shift(double* __restrict__ eps, const double* __restrict__ eps_n, Vec6 d, int64_t N) {
-    const int64_t n6 = 6 * N;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n6; i += (int64_t)gridDim.x * blockDim.x)
-        eps[i] = eps_n[i] + d.v[i / N];
+// eps = eps_n + d (start of a loading step, homogenize.py:439); n per component
+__global__ void k_shift(double* __restrict__ eps, const double* __restrict__ eps_n, Vec6 d, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) eps[c * n + i] = eps_n[c * n + i] + d.v[c];
 }
 
-struct Dims {
-    int nx, ny, nz, nzh;
-    int64_t N, Nh;
-};
-
-__device__ __forceinline__ void bin_coords(const Dims& d, int64_t q, int& ix, int& iy, int& iz) {
-    iz = (int)(q % d.nzh);
-    const int64_t r = q / d.nzh;
-    iy = (int)(r % d.ny);
-    ix = (int)(r / d.ny);
-}
-
-// K2: residual partials + Green update for every bin but the origin.
-// shat: rfft(sigma) in, ehat'/N out;  ehat: rfft(eps) in, ehat' out.
-__global__ void __launch_bounds__(kRedThreads) k_fourier(Dims d, RefMat ref, cufftDoubleComplex* __restrict__ shat,
-                                                         cufftDoubleComplex* __restrict__ ehat, double* __restrict__ partial,
+// K2: residual partials + Green update for every bin of the slab but the
+// global origin.  Block b handles part (b % kParts) of ky plane (b / kParts);
+// its partial goes to red[(y0 + kyl) * kParts + part].
+// S: rfft(sigma) in, ehat'/N out;  ehat: rfft(eps) in, ehat' out.
+__global__ void __launch_bounds__(kRedThreads) k_fourier(Spec sp, RefMat ref, double2* __restrict__ S,
+                                                         double2* __restrict__ ehat, double* __restrict__ red,
                                                          int update) {
     __shared__ double sh[kRedThreads / 32];
-    const double invN = 1.0 / (double)d.N;
+    const int kyl = blockIdx.x / kParts, part = blockIdx.x % kParts;
+    const int ky = sp.y0 + kyl;
+    const int64_t nb = (int64_t)sp.nx * sp.nzh;
+    const int64_t lo = nb * part / kParts, hi = nb * (part + 1) / kParts;
+    const double invN = 1.0 / (double)sp.N;
     double acc = 0.0;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < d.Nh; q += (int64_t)gridDim.x * blockDim.x) {
-        int ix, iy, iz;
-        bin_coords(d, q, ix, iy, iz);
-        const Bin b = make_bin(ix, iy, iz, d.nx, d.ny, d.nz);
+    for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+        const int kx = (int)(j / sp.nzh), kz = (int)(j % sp.nzh);
+        const int64_t q = kx * sp.xs + (int64_t)kyl * sp.nzh + kz;
+        const Bin b = make_bin(kx, ky, kz, sp.nx, sp.ny, sp.nz);
         cplx s[6];
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-            const cufftDoubleComplex v = shat[c * d.Nh + q];
+            const double2 v = S[c * sp.cs + q];
             s[c] = cplx{v.x, v.y};
         }
-        if (!b.zero) acc += rfft_weight(iz, d.nz) * traction_sq(b, s);
+        if (!b.zero) acc += rfft_weight(kz, sp.nz) * traction_sq(b, s);
         if (update && !b.zero) {
             double er[6], ei[6], cr[6], ci[6], tr[6], ti[6], outr[6], outi[6];
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
-                const cufftDoubleComplex v = ehat[c * d.Nh + q];
+                const double2 v = ehat[c * sp.cs + q];
                 er[c] = v.x;
                 ei[c] = v.y;
             }
@@ -124,59 +152,92 @@ __global__ void __launch_bounds__(kRedThreads) k_fourier(Dims d, RefMat ref, cuf
             green_apply_real(ref, b, ti, outi);
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
-                ehat[c * d.Nh + q] = make_cuDoubleComplex(outr[c], outi[c]);
-                shat[c * d.Nh + q] = make_cuDoubleComplex(outr[c] * invN, outi[c] * invN);
+                ehat[c * sp.cs + q] = make_double2(outr[c], outi[c]);
+                S[c * sp.cs + q] = make_double2(outr[c] * invN, outi[c] * invN);
             }
         }
     }
     const double t = block_sum(acc, sh);
-    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+    if (threadIdx.x == 0) red[(int64_t)ky * kParts + part] = t;
 }
 
-// out[0] = sum of partials (fixed order), out[1..6] = Re shat(0) (= N sigma_bar),
-// out[7] = material status flags
-__global__ void k_finish(const double* __restrict__ partial, int np, const cufftDoubleComplex* __restrict__ shat,
-                         int64_t Nh, const uint32_t* __restrict__ flags, double* __restrict__ out) {
-    __shared__ double sh[32];
-    double v = 0.0;
-    for (int i = threadIdx.x; i < np; i += blockDim.x) v += partial[i];
-    const double t = block_sum(v, sh);
-    if (threadIdx.x == 0) {
-        out[0] = t;
-        for (int c = 0; c < 6; ++c) out[1 + c] = shat[c * Nh].x;
-        out[7] = (double)(flags ? *flags : 0u);
-    }
+// red[P*ny + 0..5] = Re S(origin) on the origin's owner (else 0),
+// red[P*ny + 6] = 1 if any material point failed
+__global__ void k_finish(const double2* __restrict__ S, int64_t cs, int owner, const uint32_t* __restrict__ flags,
+                         double* __restrict__ red, int64_t off) {
+    const int c = threadIdx.x;
+    if (c < 6) red[off + c] = owner ? S[c * cs].x : 0.0;
+    if (c == 6) red[off + 6] = (flags && (*flags & AM_VOXEL_NEWTON_FAILED)) ? 1.0 : 0.0;
+    if (c == 7) red[off + 7] = 0.0;
 }
 
-// origin bin of the update: ehat(0) = N ebar, Z2D input ebar
-__global__ void k_origin(cufftDoubleComplex* shat, cufftDoubleComplex* ehat, int64_t Nh, Vec6 ebar, double N) {
+// origin bin of the update: ehat(0) = N ebar, inverse-FFT input ebar
+__global__ void k_origin(double2* S, double2* ehat, int64_t cs, Vec6 ebar, double N) {
     const int c = threadIdx.x;
     if (c < 6) {
-        ehat[c * Nh] = make_cuDoubleComplex(ebar.v[c] * N, 0.0);
-        shat[c * Nh] = make_cuDoubleComplex(ebar.v[c], 0.0);
+        ehat[c * cs] = make_double2(ebar.v[c] * N, 0.0);
+        S[c * cs] = make_double2(ebar.v[c], 0.0);
     }
 }
 
-// standalone Green application on a spectrum (GreenOperator.apply): every
-// bin, the origin -> 0, output scaled by 1/N for the Z2D
-__global__ void k_green(Dims d, RefMat ref, cufftDoubleComplex* __restrict__ h) {
-    const double invN = 1.0 / (double)d.N;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < d.Nh; q += (int64_t)gridDim.x * blockDim.x) {
-        int ix, iy, iz;
-        bin_coords(d, q, ix, iy, iz);
-        const Bin b = make_bin(ix, iy, iz, d.nx, d.ny, d.nz);
+// forward transpose, pack: 2-D spectra P (6, nxl, ny, nzh) -> send blocks
+// [dest j][xl][c][ky - y0_j][kz] (equal ky ranges nyl per slab)
+__global__ void k_pack(const double2* __restrict__ P, double2* __restrict__ send, int nxl, int ny, int nzh, int nyl) {
+    const int64_t total = (int64_t)6 * nxl * ny * nzh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        // i enumerates the send buffer: ((j * nxl + xl) * 6 + c) * nyl * nzh + kyl * nzh + kz
+        const int kz = (int)(i % nzh);
+        int64_t r = i / nzh;
+        const int kyl = (int)(r % nyl);
+        r /= nyl;
+        const int c = (int)(r % 6);
+        r /= 6;
+        const int xl = (int)(r % nxl);
+        const int j = (int)(r / nxl);
+        const int ky = j * nyl + kyl;
+        send[i] = P[((int64_t)(c * nxl + xl) * ny + ky) * nzh + kz];
+    }
+}
+
+// inverse transpose, unpack: receive blocks [src i][xl][c][kyl][kz] -> 2-D
+// spectra P (6, nxl, ny, nzh) with ky = i * nyl + kyl
+__global__ void k_unpack(const double2* __restrict__ recv, double2* __restrict__ P, int nxl, int ny, int nzh, int nyl) {
+    const int64_t total = (int64_t)6 * nxl * ny * nzh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int kz = (int)(i % nzh);
+        int64_t r = i / nzh;
+        const int kyl = (int)(r % nyl);
+        r /= nyl;
+        const int c = (int)(r % 6);
+        r /= 6;
+        const int xl = (int)(r % nxl);
+        const int src = (int)(r / nxl);
+        const int ky = src * nyl + kyl;
+        P[((int64_t)(c * nxl + xl) * ny + ky) * nzh + kz] = recv[i];
+    }
+}
+
+// standalone Green application on a single-layout spectrum (GreenOperator.apply):
+// every bin, origin -> 0, output scaled by 1/N for the Z2D
+__global__ void k_green(Spec sp, RefMat ref, double2* __restrict__ h) {
+    const double invN = 1.0 / (double)sp.N;
+    const int64_t nbins = (int64_t)sp.nx * sp.ny * sp.nzh;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nbins; q += (int64_t)gridDim.x * blockDim.x) {
+        const int kz = (int)(q % sp.nzh);
+        const int64_t r = q / sp.nzh;
+        const int ky = (int)(r % sp.ny), kx = (int)(r / sp.ny);
+        const Bin b = make_bin(kx, ky, kz, sp.nx, sp.ny, sp.nz);
         double tr[6], ti[6], outr[6], outi[6];
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-            tr[c] = h[c * d.Nh + q].x;
-            ti[c] = h[c * d.Nh + q].y;
+            tr[c] = h[c * sp.cs + q].x;
+            ti[c] = h[c * sp.cs + q].y;
         }
         green_apply_real(ref, b, tr, outr);
         green_apply_real(ref, b, ti, outi);
 #pragma unroll
         for (int c = 0; c < 6; ++c)
-            h[c * d.Nh + q] = b.zero ? make_cuDoubleComplex(0.0, 0.0)
-                                     : make_cuDoubleComplex(outr[c] * invN, outi[c] * invN);
+            h[c * sp.cs + q] = b.zero ? make_double2(0.0, 0.0) : make_double2(outr[c] * invN, outi[c] * invN);
     }
 }
 
@@ -194,7 +255,7 @@ __global__ void k_isotropic(RefMat ref, const double* __restrict__ e, double* __
 
 // K5: per-voxel tangent bounds + C sums over a chunk of tangents stored
 // C[(i*6+j)*cs + b].  Per block: [sum C (36), min kappa, max kappa,
-// min mu_lo, max mu_hi, nonfinite count] -> stats[blockIdx * 41 + ...]
+// min mu_lo, max mu_hi, non-finite count] -> stats[blockIdx * 41 + ...]
 constexpr int kStat = 41;
 __global__ void __launch_bounds__(kRedThreads) k_refstats(const double* __restrict__ C, int64_t cs, int64_t B,
                                                           DevBasis db, double* __restrict__ stats) {
@@ -227,7 +288,7 @@ __global__ void __launch_bounds__(kRedThreads) k_refstats(const double* __restri
         mhi = fmax(mhi, hi);
     }
     double* out = stats + (int64_t)blockIdx.x * kStat;
-#pragma unroll 1
+#pragma unroll
     for (int i = 0; i < 36; ++i) {
         const double t = block_sum(sum[i], sh);
         if (threadIdx.x == 0) out[i] = t;
@@ -235,8 +296,8 @@ __global__ void __launch_bounds__(kRedThreads) k_refstats(const double* __restri
     const double t = block_sum(bad, sh);
     if (threadIdx.x == 0) out[40] = t;
     // min / max are order independent
-    double vals[4] = {kmin, -kmax, mlo, -mhi};
-#pragma unroll 1
+    const double vals[4] = {kmin, -kmax, mlo, -mhi};
+#pragma unroll
     for (int v = 0; v < 4; ++v) {
         red[threadIdx.x] = vals[v];
         __syncthreads();
@@ -249,16 +310,13 @@ __global__ void __launch_bounds__(kRedThreads) k_refstats(const double* __restri
     }
 }
 
-// gather-scatter copy of a phase's C chunk into an (N, 6, 6) field is done on
-// the host (API path only)
-
 // ---------------------------------------------------------------- host helpers
 static unsigned grid_for(int64_t n, int threads = 256) {
     int64_t b = (n + threads - 1) / threads;
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)kSMs * 32));
 }
 
-// LAPACK-style dense solve with partial pivoting (numpy.linalg.solve,
+// dense solve with partial pivoting (numpy.linalg.solve / LAPACK gesv,
 // homogenize.py:463) for the <= 6x6 mixed-BC system
 static bool small_solve(int n, double* A, double* x) {
     int piv[6];
@@ -294,20 +352,17 @@ static void ref_matrix(double lam, double mu, double* C) {
     for (int i = 3; i < 6; ++i) C[i * 6 + i] = mu;
 }
 
-// ---------------------------------------------------------------- the solver
-struct Phase {
-    am_law law;
-    int m = 0;
-    int64_t count = 0;
-    int64_t* gidx = nullptr;
-    double* a_n = nullptr;
-    double* a_pend = nullptr;
-};
+static double dup_norm(const double* s) {
+    // sqrt(sigma_bar . SHEAR_DUP . sigma_bar) (homogenize.py:266, 449)
+    const double dup[6] = {1, 1, 1, 2, 2, 2};
+    double t = 0.0;
+    for (int i = 0; i < 6; ++i) t += s[i] * dup[i] * s[i];
+    return std::sqrt(t);
+}
 
 struct Stats {
     double Csum[36];
-    double kmin, kmax, mlo, mhi;
-    double bad;
+    double kmin, kmax, mlo, mhi, bad;
     void reset() {
         for (double& c : Csum) c = 0.0;
         kmin = mlo = INFINITY;
@@ -324,191 +379,344 @@ struct Stats {
     }
 };
 
+// ---------------------------------------------------------------- slabs
+struct Phase {
+    am_law law;
+    int m = 0;
+    int64_t count = 0;        // voxels of this phase in the slab
+    int64_t* gidx = nullptr;  // slab-local voxel indices (sorted)
+    double* a_n = nullptr;
+    double* a_pend = nullptr;
+};
+
+struct Slab {
+    int rank = 0;
+    int x0 = 0, nxl = 0;  // real-space x planes
+    int y0 = 0, nyl = 0;  // spectral ky planes (multi-slab layout)
+    int64_t Nl = 0;       // nxl * ny * nz
+    Spec sp{};
+    double *eps = nullptr, *eps_n = nullptr, *sigma = nullptr;
+    double2 *S = nullptr, *ehat = nullptr;   // spectra
+    double2 *P = nullptr, *X = nullptr;      // 2-D spectra / exchange buffer (multi-slab)
+    uint32_t* flags = nullptr;
+    std::vector<Phase> phases;
+};
+
 }  // namespace am
 
 struct am_solver {
-    am::Dims d{};
+    int nx = 0, ny = 0, nz = 0, nzh = 0;
+    int64_t N = 0;
     int device = 0;
     cudaStream_t stream = nullptr;
     am_cfg cfg{};
-    std::vector<am::Phase> phases;
-    double *eps = nullptr, *eps_n = nullptr, *sigma = nullptr;
-    cufftDoubleComplex *shat = nullptr, *ehat = nullptr;
-    cufftHandle r2c = 0, c2r = 0;
-    double* partial = nullptr;
-    double* dsmall = nullptr;
-    double* hsmall = nullptr;  // pinned
-    uint32_t* flags = nullptr;
-    // tangent sweep scratch
-    int64_t chunk = 0;
+    int nslabs = 1;      // global slab count
+    bool multi = false;  // slab (transpose) algorithm vs 3-D cuFFT
+    ncclComm_t comm = nullptr;  // nccl mode: this process holds one slab
+    std::vector<am::Slab> slabs;  // slabs held by this process
+    cufftHandle r3 = 0, c3 = 0;   // 3-D D2Z / Z2D (single slab)
+    cufftHandle r2 = 0, c2 = 0;   // 2-D D2Z / Z2D over (y, z), batch 6 nxl
+    cufftHandle x1 = 0;           // 1-D Z2Z over x, batch 6 nyl nzh
+    double* red = nullptr;        // reduction vectors, one per local slab, length redlen
+    double* hred = nullptr;       // pinned host copy
+    int64_t redlen = 0;
+    int64_t chunk = 0;            // tangent sweep chunk
     double* Cbuf = nullptr;
     uint8_t* status = nullptr;
     double* stats = nullptr;
-    double* hstats = nullptr;  // pinned
+    double* hstats = nullptr;
+    double* dsmall = nullptr;     // nccl reductions of the tangent statistics
     double lam = 0.0, mu = 0.0;
     double ebar_n[6] = {0, 0, 0, 0, 0, 0};
-    double ebar[6] = {0, 0, 0, 0, 0, 0};  // mean strain of the current iterate
     bool pending = false;
     am::DevBasis db = am::DevBasis::make();
-    // optional per-phase device timing of solve_step (am_solver_timing)
     bool timing = false;
     cudaEvent_t ev[6] = {};
-    double t_ms[5] = {0, 0, 0, 0, 0};  // material, d2z, fourier+reduce, z2d+origin, iterations
+    double t_ms[5] = {0, 0, 0, 0, 0};  // material, forward FFT, fourier+reduce, inverse FFT, iterations
 };
 
 namespace am {
 
-static int solver_free(am_solver* h) {
-    if (!h) return AM_OK;
+static void solver_free(am_solver* h) {
+    if (!h) return;
     cudaSetDevice(h->device);
-    for (auto& p : h->phases) {
-        cudaFree(p.gidx);
-        cudaFree(p.a_n);
-        cudaFree(p.a_pend);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (auto& s : h->slabs) {
+        for (auto& p : s.phases) {
+            cudaFree(p.gidx);
+            cudaFree(p.a_n);
+            cudaFree(p.a_pend);
+        }
+        cudaFree(s.eps); cudaFree(s.eps_n); cudaFree(s.sigma);
+        cudaFree(s.S); cudaFree(s.ehat); cudaFree(s.P); cudaFree(s.X); cudaFree(s.flags);
     }
-    cudaFree(h->eps); cudaFree(h->eps_n); cudaFree(h->sigma);
-    cudaFree(h->shat); cudaFree(h->ehat);
-    cudaFree(h->partial); cudaFree(h->dsmall); cudaFreeHost(h->hsmall); cudaFree(h->flags);
-    cudaFree(h->Cbuf); cudaFree(h->status); cudaFree(h->stats); cudaFreeHost(h->hstats);
+    cudaFree(h->red); cudaFreeHost(h->hred);
+    cudaFree(h->Cbuf); cudaFree(h->status); cudaFree(h->stats); cudaFreeHost(h->hstats); cudaFree(h->dsmall);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
-    if (h->r2c) cufftDestroy(h->r2c);
-    if (h->c2r) cufftDestroy(h->c2r);
+    for (cufftHandle p : {h->r3, h->c3, h->r2, h->c2, h->x1})
+        if (p) cufftDestroy(p);
+    if (h->comm) ncclCommDestroy(h->comm);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
+}
+
+// ---------------------------------------------------------------- transport
+// all-to-all of equal blocks: block j of slab i's `send` -> block i of slab j's `recv`
+static int alltoall(am_solver* h, double2* Slab::*send, double2* Slab::*recv, size_t blk) {
+    if (h->comm) {
+        Slab& s = h->slabs[0];
+        AM_NCCL(ncclAlltoAll(s.*send, s.*recv, 2 * blk, ncclDouble, h->comm, h->stream));
+        return AM_OK;
+    }
+    for (auto& si : h->slabs)
+        for (auto& sj : h->slabs)
+            AM_CUDA(cudaMemcpyAsync(sj.*recv + (size_t)si.rank * blk, si.*send + (size_t)sj.rank * blk,
+                                    blk * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
     return AM_OK;
 }
 
-// K1 over every phase: sigma field and pending states from (eps_n, a_n, eps)
-static int material_sweep(am_solver* h, double dt) {
-    AM_CUDA(cudaMemsetAsync(h->flags, 0, sizeof(uint32_t), h->stream));
-    for (auto& p : h->phases) {
-        if (!p.count) continue;
-        KArgs k{};
-        k.B = p.count;
-        k.gidx = p.gidx;
-        k.eps_n = h->eps_n; k.eps_np1 = h->eps; k.a_n = p.a_n; k.dt = nullptr; k.dt_scalar = dt;
-        k.le = {h->d.N, 1}; k.la = {p.count, 1}; k.lc = {0, 0};
-        k.sigma = h->sigma; k.a_out = p.a_pend; k.C = nullptr;
-        k.iters = nullptr; k.status = nullptr; k.flags = h->flags;
-        k.ncfg = newton_cfg(&h->cfg);
-        AM_TRY(launch_material(&p.law, k, h->stream));
+// element-wise sum of every slab's reduction vector -> host (disjoint
+// supports, so the sum is exact and independent of the slab count)
+static int reduce_to_host(am_solver* h, double* out) {
+    const int64_t L = h->redlen;
+    if (h->comm) AM_NCCL(ncclAllReduce(h->red, h->red, L, ncclDouble, ncclSum, h->comm, h->stream));
+    const size_t nvec = h->comm ? 1 : h->slabs.size();
+    AM_CUDA(cudaMemcpyAsync(h->hred, h->red, sizeof(double) * L * nvec, cudaMemcpyDeviceToHost, h->stream));
+    AM_CUDA(cudaStreamSynchronize(h->stream));
+    for (int64_t i = 0; i < L; ++i) {
+        double v = 0.0;
+        for (size_t s = 0; s < nvec; ++s) v += h->hred[s * L + i];
+        out[i] = v;
     }
     return AM_OK;
 }
 
-static int fft_forward(am_solver* h, double* field, cufftDoubleComplex* out) {
-    AM_CUFFT(cufftExecD2Z(h->r2c, field, out));
+// ---------------------------------------------------------------- transforms
+// rfft of a real slab field -> spectrum buffer `dst` (S or ehat) of every slab
+static int forward(am_solver* h, double* Slab::*field, double2* Slab::*dst) {
+    if (!h->multi) {
+        Slab& s = h->slabs[0];
+        AM_CUFFT(cufftExecD2Z(h->r3, s.*field, s.*dst));
+        return AM_OK;
+    }
+    for (auto& s : h->slabs) {
+        AM_CUFFT(cufftExecD2Z(h->r2, s.*field, s.P));
+        k_pack<<<grid_for((int64_t)6 * s.nxl * h->ny * h->nzh), 256, 0, h->stream>>>(s.P, s.X, s.nxl, h->ny, h->nzh,
+                                                                                      s.nyl);
+        AM_CUDA(cudaGetLastError());
+    }
+    AM_TRY(alltoall(h, &Slab::X, dst, (size_t)6 * h->slabs[0].nxl * h->slabs[0].nyl * h->nzh));
+    for (auto& s : h->slabs) AM_CUFFT(cufftExecZ2Z(h->x1, s.*dst, s.*dst, CUFFT_FORWARD));
     return AM_OK;
 }
 
-static int fft_inverse(am_solver* h, cufftDoubleComplex* in, double* field) {
-    AM_CUFFT(cufftExecZ2D(h->c2r, in, field));
+// real field of every slab = irfft of the spectrum buffer `src` (destroyed)
+static int inverse(am_solver* h, double2* Slab::*src, double* Slab::*field) {
+    if (!h->multi) {
+        Slab& s = h->slabs[0];
+        AM_CUFFT(cufftExecZ2D(h->c3, s.*src, s.*field));
+        return AM_OK;
+    }
+    for (auto& s : h->slabs) AM_CUFFT(cufftExecZ2Z(h->x1, s.*src, s.*src, CUFFT_INVERSE));
+    AM_TRY(alltoall(h, src, &Slab::X, (size_t)6 * h->slabs[0].nxl * h->slabs[0].nyl * h->nzh));
+    for (auto& s : h->slabs) {
+        k_unpack<<<grid_for((int64_t)6 * s.nxl * h->ny * h->nzh), 256, 0, h->stream>>>(s.X, s.P, s.nxl, h->ny,
+                                                                                        h->nzh, s.nyl);
+        AM_CUDA(cudaGetLastError());
+        AM_CUFFT(cufftExecZ2D(h->c2, s.P, s.*field));
+    }
     return AM_OK;
 }
 
-// residual of the current sigma (whose rfft is in shat) and, when `update`,
-// the Green update of every bin but the origin; returns the 8 host values
-static int fourier_pass(am_solver* h, bool update, double* out8) {
-    RefMat ref = RefMat::make(h->lam, h->mu);
-    k_fourier<<<kRedBlocks, kRedThreads, 0, h->stream>>>(h->d, ref, h->shat, h->ehat, h->partial, update ? 1 : 0);
-    AM_CUDA(cudaGetLastError());
-    k_finish<<<1, 1024, 0, h->stream>>>(h->partial, kRedBlocks, h->shat, h->d.Nh, h->flags, h->dsmall);
-    AM_CUDA(cudaGetLastError());
-    AM_CUDA(cudaMemcpyAsync(h->hsmall, h->dsmall, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    AM_CUDA(cudaStreamSynchronize(h->stream));
-    std::memcpy(out8, h->hsmall, 8 * sizeof(double));
+// K1 over every phase of every local slab
+static int material_sweep(am_solver* h, double dt) {
+    for (auto& s : h->slabs) {
+        AM_CUDA(cudaMemsetAsync(s.flags, 0, sizeof(uint32_t), h->stream));
+        for (auto& p : s.phases) {
+            if (!p.count) continue;
+            KArgs k{};
+            k.B = p.count;
+            k.gidx = p.gidx;
+            k.eps_n = s.eps_n; k.eps_np1 = s.eps; k.a_n = p.a_n; k.dt = nullptr; k.dt_scalar = dt;
+            k.le = {s.Nl, 1}; k.la = {p.count, 1}; k.lc = {0, 0};
+            k.sigma = s.sigma; k.a_out = p.a_pend; k.C = nullptr;
+            k.iters = nullptr; k.status = nullptr; k.flags = s.flags;
+            k.ncfg = newton_cfg(&h->cfg);
+            AM_TRY(launch_material(&p.law, k, h->stream));
+        }
+    }
     return AM_OK;
 }
 
-static double dup_norm(const double* s) {
-    // sqrt(sigma_bar . SHEAR_DUP . sigma_bar) (homogenize.py:266, 449)
-    const double dup[6] = {1, 1, 1, 2, 2, 2};
-    double t = 0.0;
-    for (int i = 0; i < 6; ++i) t += s[i] * dup[i] * s[i];
-    return std::sqrt(t);
+// residual partials (+ update) of every slab -> host vector
+// [ny * kParts partials | Re S(origin) (6) | any Newton failure | 0]
+static int fourier_pass(am_solver* h, bool update, std::vector<double>& out) {
+    const RefMat ref = RefMat::make(h->lam, h->mu);
+    const int64_t L = h->redlen;
+    AM_CUDA(cudaMemsetAsync(h->red, 0, sizeof(double) * L * h->slabs.size(), h->stream));
+    for (size_t i = 0; i < h->slabs.size(); ++i) {
+        Slab& s = h->slabs[i];
+        double* red = h->red + (int64_t)i * L;
+        k_fourier<<<s.sp.nyl * kParts, kRedThreads, 0, h->stream>>>(s.sp, ref, s.S, s.ehat, red, update ? 1 : 0);
+        AM_CUDA(cudaGetLastError());
+        k_finish<<<1, 32, 0, h->stream>>>(s.S, s.sp.cs, s.y0 == 0 ? 1 : 0, s.flags, red, (int64_t)h->ny * kParts);
+        AM_CUDA(cudaGetLastError());
+    }
+    out.resize(L);
+    return reduce_to_host(h, out.data());
 }
 
 }  // namespace am
 
 using namespace am;
 
-extern "C" int am_solver_create(int nx, int ny, int nz, const uint8_t* ids, int nmat, const am_law* laws,
-                                const am_cfg* cfg, am_solver** out) {
-    if (!out || !ids || !laws || nmat <= 0 || nx <= 0 || ny <= 0 || nz <= 0)
+// ---------------------------------------------------------------- creation
+static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, const am_law* laws, const am_cfg* cfg,
+                        int nslabs, int first, int nlocal, ncclComm_t comm, am_solver** out) {
+    if (!out || !ids || !laws || nmat <= 0 || nx <= 0 || ny <= 0 || nz <= 0 || nslabs <= 0)
         return fail(AM_ERR_ARG, "am_solver_create: bad arguments");
+    if (nslabs > 1 && (nx % nslabs || ny % nslabs))
+        return fail(AM_ERR_ARG, "slab count %d must divide nx = %d and ny = %d", nslabs, nx, ny);
     AM_TRY(check_cfg(cfg));
     for (int i = 0; i < nmat; ++i) AM_TRY(check_law(&laws[i]));
     const int64_t N = (int64_t)nx * ny * nz;
-    std::vector<std::vector<int64_t>> idx(nmat);
-    for (int64_t i = 0; i < N; ++i) {
+    for (int64_t i = 0; i < N; ++i)
         if (ids[i] >= nmat) return fail(AM_ERR_ARG, "material id exceeds material table");
-        idx[ids[i]].push_back(i);
-    }
     auto* h = new am_solver();
-    int rc = AM_OK;
     auto bail = [&](int code) {
+        if (comm && h->comm == nullptr) ncclCommDestroy(comm);
         solver_free(h);
         return code;
     };
-    if (cudaGetDevice(&h->device) != cudaSuccess) return bail(fail(AM_ERR_CUDA, "no CUDA device"));
-    h->d = Dims{nx, ny, nz, nz / 2 + 1, N, (int64_t)nx * ny * (nz / 2 + 1)};
-    h->cfg = *cfg;
-#define AMC(expr)                                                                                     \
-    do {                                                                                              \
-        cudaError_t _e = (expr);                                                                      \
+#define AMC(expr)                                                                                       \
+    do {                                                                                                \
+        cudaError_t _e = (expr);                                                                        \
         if (_e != cudaSuccess) return bail(fail(AM_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e))); \
     } while (0)
+    AMC(cudaGetDevice(&h->device));
+    h->comm = comm;
+    h->nx = nx; h->ny = ny; h->nz = nz; h->nzh = nz / 2 + 1; h->N = N;
+    h->cfg = *cfg;
+    h->nslabs = nslabs;
+    h->multi = nslabs > 1 || comm != nullptr;  // nccl mode always transposes (same bits for every rank count)
     AMC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-    AMC(cudaMalloc(&h->eps, sizeof(double) * 6 * N));
-    AMC(cudaMalloc(&h->eps_n, sizeof(double) * 6 * N));
-    AMC(cudaMalloc(&h->sigma, sizeof(double) * 6 * N));
-    AMC(cudaMemset(h->eps_n, 0, sizeof(double) * 6 * N));
-    AMC(cudaMemset(h->eps, 0, sizeof(double) * 6 * N));
-    AMC(cudaMemset(h->sigma, 0, sizeof(double) * 6 * N));
-    AMC(cudaMalloc(&h->shat, sizeof(cufftDoubleComplex) * 6 * h->d.Nh));
-    AMC(cudaMalloc(&h->ehat, sizeof(cufftDoubleComplex) * 6 * h->d.Nh));
-    AMC(cudaMalloc(&h->partial, sizeof(double) * kRedBlocks));
-    AMC(cudaMalloc(&h->dsmall, sizeof(double) * 8));
-    AMC(cudaMallocHost(&h->hsmall, sizeof(double) * 8));
-    AMC(cudaMalloc(&h->flags, sizeof(uint32_t)));
-    h->chunk = std::min<int64_t>(N, int64_t(1) << 22);
+    const int nxl = nx / nslabs, nyl = ny / nslabs;
+    const int64_t Nl = (int64_t)nxl * ny * nz;
+    const int64_t spec = (int64_t)6 * nxl * ny * h->nzh;  // complex elements per slab spectrum
+    for (int r = first; r < first + nlocal; ++r) {
+        Slab s;
+        s.rank = r;
+        s.x0 = r * nxl; s.nxl = nxl; s.y0 = h->multi ? r * nyl : 0; s.nyl = h->multi ? nyl : ny; s.Nl = Nl;
+        s.sp = h->multi ? spec_slab(nx, ny, nz, s.y0, nyl) : spec_single(nx, ny, nz);
+        h->slabs.push_back(s);
+        Slab& sl = h->slabs.back();
+        AMC(cudaMalloc(&sl.eps, sizeof(double) * 6 * Nl));
+        AMC(cudaMalloc(&sl.eps_n, sizeof(double) * 6 * Nl));
+        AMC(cudaMalloc(&sl.sigma, sizeof(double) * 6 * Nl));
+        AMC(cudaMemset(sl.eps, 0, sizeof(double) * 6 * Nl));
+        AMC(cudaMemset(sl.eps_n, 0, sizeof(double) * 6 * Nl));
+        AMC(cudaMemset(sl.sigma, 0, sizeof(double) * 6 * Nl));
+        AMC(cudaMalloc(&sl.S, sizeof(double2) * spec));
+        AMC(cudaMalloc(&sl.ehat, sizeof(double2) * spec));
+        if (h->multi) {
+            AMC(cudaMalloc(&sl.P, sizeof(double2) * spec));
+            AMC(cudaMalloc(&sl.X, sizeof(double2) * spec));
+        }
+        AMC(cudaMalloc(&sl.flags, sizeof(uint32_t)));
+        AMC(cudaMemset(sl.flags, 0, sizeof(uint32_t)));
+        // phases: slab-local sorted indices (the global order restricted to the slab)
+        std::vector<std::vector<int64_t>> idx(nmat);
+        const uint8_t* sid = ids + (int64_t)sl.x0 * ny * nz;
+        for (int64_t i = 0; i < Nl; ++i) idx[sid[i]].push_back(i);
+        for (int k = 0; k < nmat; ++k) {
+            Phase p;
+            p.law = laws[k];
+            p.m = law_m(&laws[k]);
+            p.count = (int64_t)idx[k].size();
+            sl.phases.push_back(p);
+            Phase& ph = sl.phases.back();
+            if (!ph.count) continue;
+            AMC(cudaMalloc(&ph.gidx, sizeof(int64_t) * ph.count));
+            AMC(cudaMemcpy(ph.gidx, idx[k].data(), sizeof(int64_t) * ph.count, cudaMemcpyHostToDevice));
+            if (ph.m) {
+                AMC(cudaMalloc(&ph.a_n, sizeof(double) * ph.m * ph.count));
+                AMC(cudaMalloc(&ph.a_pend, sizeof(double) * ph.m * ph.count));
+                AMC(cudaMemset(ph.a_n, 0, sizeof(double) * ph.m * ph.count));
+                AMC(cudaMemset(ph.a_pend, 0, sizeof(double) * ph.m * ph.count));
+            }
+        }
+    }
+    h->redlen = (int64_t)ny * kParts + 8;
+    AMC(cudaMalloc(&h->red, sizeof(double) * h->redlen * h->slabs.size()));
+    AMC(cudaMallocHost(&h->hred, sizeof(double) * h->redlen * h->slabs.size()));
+    h->chunk = std::min<int64_t>(Nl, int64_t(1) << 22);
     AMC(cudaMalloc(&h->Cbuf, sizeof(double) * 36 * h->chunk));
     AMC(cudaMalloc(&h->status, h->chunk));
     AMC(cudaMalloc(&h->stats, sizeof(double) * kStat * kRedBlocks));
     AMC(cudaMallocHost(&h->hstats, sizeof(double) * kStat * kRedBlocks));
-    for (int i = 0; i < nmat; ++i) {
-        Phase p;
-        p.law = laws[i];
-        p.m = law_m(&laws[i]);
-        p.count = (int64_t)idx[i].size();
-        if (p.count) {
-            AMC(cudaMalloc(&p.gidx, sizeof(int64_t) * p.count));
-            AMC(cudaMemcpy(p.gidx, idx[i].data(), sizeof(int64_t) * p.count, cudaMemcpyHostToDevice));
-            if (p.m) {
-                AMC(cudaMalloc(&p.a_n, sizeof(double) * p.m * p.count));
-                AMC(cudaMalloc(&p.a_pend, sizeof(double) * p.m * p.count));
-                AMC(cudaMemset(p.a_n, 0, sizeof(double) * p.m * p.count));
-                AMC(cudaMemset(p.a_pend, 0, sizeof(double) * p.m * p.count));
-            }
-        }
-        h->phases.push_back(p);
-    }
+    AMC(cudaMalloc(&h->dsmall, sizeof(double) * 64));
 #undef AMC
-    long long n3[3] = {nx, ny, nz};
     size_t ws = 0;
-    if (cufftCreate(&h->r2c) != CUFFT_SUCCESS || cufftCreate(&h->c2r) != CUFFT_SUCCESS)
-        return bail(fail(AM_ERR_CUDA, "cufftCreate failed"));
-    if (cufftMakePlanMany64(h->r2c, 3, n3, nullptr, 1, N, nullptr, 1, h->d.Nh, CUFFT_D2Z, 6, &ws) != CUFFT_SUCCESS ||
-        cufftMakePlanMany64(h->c2r, 3, n3, nullptr, 1, h->d.Nh, nullptr, 1, N, CUFFT_Z2D, 6, &ws) != CUFFT_SUCCESS)
-        return bail(fail(AM_ERR_CUDA, "cufft plan creation failed for %dx%dx%d", nx, ny, nz));
-    cufftSetStream(h->r2c, h->stream);
-    cufftSetStream(h->c2r, h->stream);
+    auto plan = [&](cufftHandle* p, int rank, long long* n, long long* inembed, long long istride, long long idist,
+                    long long* onembed, long long ostride, long long odist, cufftType t, long long batch) -> bool {
+        return cufftCreate(p) == CUFFT_SUCCESS &&
+               cufftMakePlanMany64(*p, rank, n, inembed, istride, idist, onembed, ostride, odist, t, batch, &ws) ==
+                   CUFFT_SUCCESS &&
+               cufftSetStream(*p, h->stream) == CUFFT_SUCCESS;
+    };
+    bool ok;
+    if (!h->multi) {
+        long long n3[3] = {nx, ny, nz};
+        ok = plan(&h->r3, 3, n3, nullptr, 1, N, nullptr, 1, (long long)nx * ny * h->nzh, CUFFT_D2Z, 6) &&
+             plan(&h->c3, 3, n3, nullptr, 1, (long long)nx * ny * h->nzh, nullptr, 1, N, CUFFT_Z2D, 6);
+    } else {
+        long long n2[2] = {ny, nz};
+        long long n1[1] = {nx};
+        const long long bx = (long long)6 * nyl * h->nzh;  // x stride = batch of the 1-D transforms
+        ok = plan(&h->r2, 2, n2, nullptr, 1, (long long)ny * nz, nullptr, 1, (long long)ny * h->nzh, CUFFT_D2Z,
+                  6LL * nxl) &&
+             plan(&h->c2, 2, n2, nullptr, 1, (long long)ny * h->nzh, nullptr, 1, (long long)ny * nz, CUFFT_Z2D,
+                  6LL * nxl) &&
+             plan(&h->x1, 1, n1, n1, bx, 1, n1, bx, 1, CUFFT_Z2Z, bx);
+    }
+    if (!ok) return bail(fail(AM_ERR_CUDA, "cufft plan creation failed for %dx%dx%d / %d slabs", nx, ny, nz, nslabs));
     *out = h;
-    return rc;
+    return AM_OK;
 }
 
-extern "C" int am_solver_destroy(am_solver* h) { return solver_free(h); }
+extern "C" int am_solver_create(int nx, int ny, int nz, const uint8_t* ids, int nmat, const am_law* laws,
+                                const am_cfg* cfg, am_solver** out) {
+    return solver_build(nx, ny, nz, ids, nmat, laws, cfg, 1, 0, 1, nullptr, out);
+}
+
+extern "C" int am_solver_create_slabs(int nx, int ny, int nz, const uint8_t* ids, int nmat, const am_law* laws,
+                                      const am_cfg* cfg, int nslabs, am_solver** out) {
+    return solver_build(nx, ny, nz, ids, nmat, laws, cfg, nslabs, 0, nslabs, nullptr, out);
+}
+
+extern "C" int am_nccl_unique_id(void* id128) {
+    if (!id128) return fail(AM_ERR_ARG, "null id buffer");
+    ncclUniqueId id;
+    AM_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof(id));
+    return AM_OK;
+}
+
+extern "C" int am_solver_create_nccl(int nx, int ny, int nz, const uint8_t* ids, int nmat, const am_law* laws,
+                                     const am_cfg* cfg, const void* id128, int rank, int nranks, am_solver** out) {
+    if (!id128 || rank < 0 || rank >= nranks) return fail(AM_ERR_ARG, "bad rank / id");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t comm = nullptr;
+    AM_NCCL(ncclCommInitRank(&comm, nranks, id, rank));
+    return solver_build(nx, ny, nz, ids, nmat, laws, cfg, nranks, rank, 1, comm, out);
+}
+
+extern "C" int am_solver_destroy(am_solver* h) {
+    solver_free(h);
+    return AM_OK;
+}
 
 extern "C" int am_solver_set_reference(am_solver* h, double lam, double mu) {
     if (!h) return fail(AM_ERR_ARG, "null solver");
@@ -530,25 +738,35 @@ extern "C" int am_solver_set_mean(am_solver* h, const double* ebar_n) {
     return AM_OK;
 }
 
+extern "C" int am_solver_layout(am_solver* h, int* nslabs, int* first, int* nlocal) {
+    if (!h) return fail(AM_ERR_ARG, "null solver");
+    if (nslabs) *nslabs = h->nslabs;
+    if (first) *first = h->slabs[0].rank;
+    if (nlocal) *nlocal = (int)h->slabs.size();
+    return AM_OK;
+}
+
+// ---------------------------------------------------------------- solve
 extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, double dt, const uint8_t* free_mask,
                                     double tol, int max_iterations, am_stepinfo* info, double* history,
                                     int history_cap) {
     if (!h || !ebar_target || !info) return fail(AM_ERR_ARG, "am_solver_solve_step: bad arguments");
     AM_CUDA(cudaSetDevice(h->device));
-    const Dims& d = h->d;
-    bool free[6];
+    bool fr[6];
     int nf = 0, fi[6];
     for (int i = 0; i < 6; ++i) {
-        free[i] = free_mask ? free_mask[i] != 0 : false;
-        if (free[i]) fi[nf++] = i;
+        fr[i] = free_mask ? free_mask[i] != 0 : false;
+        if (fr[i]) fi[nf++] = i;
     }
     double ebar[6];
-    for (int i = 0; i < 6; ++i) ebar[i] = free[i] ? h->ebar_n[i] : ebar_target[i];  // homogenize.py:436-437
+    for (int i = 0; i < 6; ++i) ebar[i] = fr[i] ? h->ebar_n[i] : ebar_target[i];  // homogenize.py:436-437
     Vec6 shift;
     for (int i = 0; i < 6; ++i) shift.v[i] = ebar[i] - h->ebar_n[i];
-    k_shift<<<grid_for(6 * d.N), 256, 0, h->stream>>>(h->eps, h->eps_n, shift, d.N);
-    AM_CUDA(cudaGetLastError());
-    AM_TRY(fft_forward(h, h->eps, h->ehat));
+    for (auto& s : h->slabs) {
+        k_shift<<<grid_for(s.Nl), 256, 0, h->stream>>>(s.eps, s.eps_n, shift, s.Nl);
+        AM_CUDA(cudaGetLastError());
+    }
+    AM_TRY(forward(h, &Slab::eps, &Slab::ehat));
     double Cff[36];
     {
         double C0[36];
@@ -560,7 +778,9 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
     info->converged = 0;
     info->residual = 0.0;
     info->mean_substeps = 1.0;  // implicit Euler: one substep per voxel (evaluator.py:130)
-    const double Nd = (double)d.N;
+    const double Nd = (double)h->N;
+    const int64_t P = (int64_t)h->ny * kParts;
+    std::vector<double> o;
     auto mark = [&](int i) -> int {
         if (h->timing) AM_CUDA(cudaEventRecord(h->ev[i], h->stream));
         return AM_OK;
@@ -575,9 +795,8 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
         AM_TRY(mark(0));
         AM_TRY(material_sweep(h, dt));
         AM_TRY(mark(1));
-        AM_TRY(fft_forward(h, h->sigma, h->shat));
+        AM_TRY(forward(h, &Slab::sigma, &Slab::S));
         AM_TRY(mark(2));
-        double o[8];
         AM_TRY(fourier_pass(h, true, o));  // synchronises the stream
         if (h->timing) {
             AM_CUDA(cudaEventRecord(h->ev[3], h->stream));
@@ -587,15 +806,17 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
             AM_TRY(acc(2, 3, 2));
             h->t_ms[4] += 1.0;
         }
-        if ((uint32_t)o[7] & AM_VOXEL_NEWTON_FAILED) {
+        if (o[P + 6] != 0.0) {
             info->iterations = it;
             return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel (iteration %d)", it);
         }
+        double fsum = 0.0;
+        for (int64_t i = 0; i < P; ++i) fsum += o[i];  // fixed order: ky plane, then part
         double sbar[6];
-        for (int i = 0; i < 6; ++i) sbar[i] = o[1 + i] / Nd;
+        for (int i = 0; i < 6; ++i) sbar[i] = o[P + i] / Nd;
         // equilibrium_residual (homogenize.py:264-267)
         const double scale = std::max(dup_norm(sbar), 1e-300);
-        const double res = std::sqrt(o[0] / (Nd * Nd)) / scale;
+        const double res = std::sqrt(fsum / (Nd * Nd)) / scale;
         double res_bc = 0.0;
         if (nf) {
             double t = 0.0;
@@ -613,7 +834,6 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
         if (res < tol && res_bc < tol) {  // strict (homogenize.py:454)
             info->converged = 1;
             h->pending = true;
-            std::memcpy(h->ebar, ebar, sizeof(ebar));
             return AM_OK;
         }
         if (nf) {  // mixed BC (homogenize.py:462-464)
@@ -623,19 +843,21 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
             if (!small_solve(nf, A, x)) return fail(AM_ERR_SINGULAR, "singular reference block");
             for (int a = 0; a < nf; ++a) ebar[fi[a]] += x[a];
         }
+        AM_TRY(mark(4));
         Vec6 eb;
         for (int i = 0; i < 6; ++i) eb.v[i] = ebar[i];
-        AM_TRY(mark(4));
-        k_origin<<<1, 32, 0, h->stream>>>(h->shat, h->ehat, d.Nh, eb, Nd);
-        AM_CUDA(cudaGetLastError());
-        AM_TRY(fft_inverse(h, h->shat, h->eps));
+        for (auto& s : h->slabs)
+            if (s.y0 == 0) {
+                k_origin<<<1, 32, 0, h->stream>>>(s.S, s.ehat, s.sp.cs, eb, Nd);
+                AM_CUDA(cudaGetLastError());
+            }
+        AM_TRY(inverse(h, &Slab::S, &Slab::eps));
         if (h->timing) {
             AM_TRY(mark(5));
             AM_CUDA(cudaEventSynchronize(h->ev[5]));
             AM_TRY(acc(4, 5, 3));
         }
     }
-    std::memcpy(h->ebar, ebar, sizeof(ebar));
     return fail(AM_ERR_NOT_CONVERGED, "basic scheme did not converge in %d iterations (last residual %.3e)",
                 max_iterations, info->residual);
 }
@@ -644,10 +866,12 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
 extern "C" int am_solver_commit(am_solver* h, const double* ebar) {
     if (!h) return fail(AM_ERR_ARG, "null solver");
     AM_CUDA(cudaSetDevice(h->device));
-    AM_CUDA(cudaMemcpyAsync(h->eps_n, h->eps, sizeof(double) * 6 * h->d.N, cudaMemcpyDeviceToDevice, h->stream));
+    for (auto& s : h->slabs)
+        AM_CUDA(cudaMemcpyAsync(s.eps_n, s.eps, sizeof(double) * 6 * s.Nl, cudaMemcpyDeviceToDevice, h->stream));
     if (ebar) std::memcpy(h->ebar_n, ebar, sizeof(h->ebar_n));
     if (h->pending) {
-        for (auto& p : h->phases) std::swap(p.a_n, p.a_pend);
+        for (auto& s : h->slabs)
+            for (auto& p : s.phases) std::swap(p.a_n, p.a_pend);
         h->pending = false;
     }
     AM_CUDA(cudaStreamSynchronize(h->stream));
@@ -660,68 +884,105 @@ extern "C" int am_solver_evaluate(am_solver* h, double dt) {
     if (!h) return fail(AM_ERR_ARG, "null solver");
     AM_CUDA(cudaSetDevice(h->device));
     AM_TRY(material_sweep(h, dt));
-    uint32_t f = 0;
-    AM_CUDA(cudaMemcpyAsync(&f, h->flags, sizeof(f), cudaMemcpyDeviceToHost, h->stream));
-    AM_CUDA(cudaStreamSynchronize(h->stream));
+    double bad = 0.0;
+    for (auto& s : h->slabs) {
+        uint32_t f = 0;
+        AM_CUDA(cudaMemcpyAsync(&f, s.flags, sizeof(f), cudaMemcpyDeviceToHost, h->stream));
+        AM_CUDA(cudaStreamSynchronize(h->stream));
+        if (f & AM_VOXEL_NEWTON_FAILED) bad = 1.0;
+    }
+    if (h->comm) {
+        AM_CUDA(cudaMemcpyAsync(h->dsmall, &bad, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        AM_NCCL(ncclAllReduce(h->dsmall, h->dsmall, 1, ncclDouble, ncclMax, h->comm, h->stream));
+        AM_CUDA(cudaMemcpyAsync(&bad, h->dsmall, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        AM_CUDA(cudaStreamSynchronize(h->stream));
+    }
     h->pending = true;
-    if (f & AM_VOXEL_NEWTON_FAILED) return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
+    if (bad != 0.0) return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
     return AM_OK;
 }
 
 // Tangent sweep of the current eps from the committed state (the
 // evaluate_field(want_tangent=True) of run_loading_path, homogenize.py:509)
 // fused with reference_update (homogenize.py:307-329): C is produced in
-// chunks, reduced to C_bar (36) and the spectral bounds, and never stored
-// as a field unless C_out (N, 6, 6, host) is given.  Also refreshes sigma and
-// the pending states.  lam_mu (optional) receives reference_update's result.
+// chunks and reduced to C_bar (36) and the spectral bounds; it is stored
+// only if C_out (host, (N_local, 6, 6) in voxel order of the local slabs)
+// is given.  Also refreshes sigma and the pending states.
 extern "C" int am_solver_tangent_sweep(am_solver* h, double dt, double* Cbar, double* lam_mu, double* C_out) {
     if (!h) return fail(AM_ERR_ARG, "null solver");
     AM_CUDA(cudaSetDevice(h->device));
     Stats st;
     st.reset();
     uint32_t any = 0;
-    AM_CUDA(cudaMemsetAsync(h->flags, 0, sizeof(uint32_t), h->stream));
     std::vector<double> hC;
     std::vector<int64_t> hidx;
-    for (auto& p : h->phases) {
-        if (!p.count) continue;
-        if (C_out) {
-            hidx.resize(p.count);
-            AM_CUDA(cudaMemcpy(hidx.data(), p.gidx, sizeof(int64_t) * p.count, cudaMemcpyDeviceToHost));
-        }
-        for (int64_t lo = 0; lo < p.count; lo += h->chunk) {
-            const int64_t n = std::min(h->chunk, p.count - lo);
-            KArgs k{};
-            k.B = n;
-            k.gidx = p.gidx + lo;
-            k.eps_n = h->eps_n; k.eps_np1 = h->eps;
-            k.a_n = p.m ? p.a_n + lo : nullptr;
-            k.dt = nullptr; k.dt_scalar = dt;
-            k.le = {h->d.N, 1}; k.la = {p.count, 1}; k.lc = {n, 1};
-            k.sigma = h->sigma; k.a_out = p.m ? p.a_pend + lo : nullptr; k.C = h->Cbuf;
-            k.iters = nullptr; k.status = h->status; k.flags = h->flags;
-            k.ncfg = newton_cfg(&h->cfg);
-            AM_TRY(launch_material(&p.law, k, h->stream));
-            k_refstats<<<kRedBlocks, kRedThreads, 0, h->stream>>>(h->Cbuf, n, n, h->db, h->stats);
-            AM_CUDA(cudaGetLastError());
-            AM_CUDA(cudaMemcpyAsync(h->hstats, h->stats, sizeof(double) * kStat * kRedBlocks, cudaMemcpyDeviceToHost,
-                                    h->stream));
+    int64_t vbase = 0;
+    for (auto& s : h->slabs) {
+        AM_CUDA(cudaMemsetAsync(s.flags, 0, sizeof(uint32_t), h->stream));
+        for (auto& p : s.phases) {
+            if (!p.count) continue;
             if (C_out) {
-                hC.resize((size_t)36 * n);
-                AM_CUDA(cudaMemcpyAsync(hC.data(), h->Cbuf, sizeof(double) * 36 * n, cudaMemcpyDeviceToHost, h->stream));
+                hidx.resize(p.count);
+                AM_CUDA(cudaMemcpy(hidx.data(), p.gidx, sizeof(int64_t) * p.count, cudaMemcpyDeviceToHost));
             }
-            AM_CUDA(cudaStreamSynchronize(h->stream));
-            for (int b = 0; b < kRedBlocks; ++b) st.add(h->hstats + (size_t)b * kStat);
-            if (C_out)
-                for (int64_t b = 0; b < n; ++b)
-                    for (int e = 0; e < 36; ++e) C_out[hidx[lo + b] * 36 + e] = hC[(size_t)e * n + b];
+            for (int64_t lo = 0; lo < p.count; lo += h->chunk) {
+                const int64_t n = std::min(h->chunk, p.count - lo);
+                KArgs k{};
+                k.B = n;
+                k.gidx = p.gidx + lo;
+                k.eps_n = s.eps_n; k.eps_np1 = s.eps;
+                k.a_n = p.m ? p.a_n + lo : nullptr;
+                k.dt = nullptr; k.dt_scalar = dt;
+                k.le = {s.Nl, 1}; k.la = {p.count, 1}; k.lc = {n, 1};
+                k.sigma = s.sigma; k.a_out = p.m ? p.a_pend + lo : nullptr; k.C = h->Cbuf;
+                k.iters = nullptr; k.status = h->status; k.flags = s.flags;
+                k.ncfg = newton_cfg(&h->cfg);
+                AM_TRY(launch_material(&p.law, k, h->stream));
+                k_refstats<<<kRedBlocks, kRedThreads, 0, h->stream>>>(h->Cbuf, n, n, h->db, h->stats);
+                AM_CUDA(cudaGetLastError());
+                AM_CUDA(cudaMemcpyAsync(h->hstats, h->stats, sizeof(double) * kStat * kRedBlocks,
+                                        cudaMemcpyDeviceToHost, h->stream));
+                if (C_out) {
+                    hC.resize((size_t)36 * n);
+                    AM_CUDA(cudaMemcpyAsync(hC.data(), h->Cbuf, sizeof(double) * 36 * n, cudaMemcpyDeviceToHost,
+                                            h->stream));
+                }
+                AM_CUDA(cudaStreamSynchronize(h->stream));
+                for (int b = 0; b < kRedBlocks; ++b) st.add(h->hstats + (size_t)b * kStat);
+                if (C_out)
+                    for (int64_t b = 0; b < n; ++b)
+                        for (int e = 0; e < 36; ++e) C_out[(vbase + hidx[lo + b]) * 36 + e] = hC[(size_t)e * n + b];
+            }
         }
+        uint32_t f = 0;
+        AM_CUDA(cudaMemcpy(&f, s.flags, sizeof(f), cudaMemcpyDeviceToHost));
+        any |= f;
+        vbase += s.Nl;
     }
-    AM_CUDA(cudaMemcpy(&any, h->flags, sizeof(any), cudaMemcpyDeviceToHost));
+    if (h->comm) {
+        // combine across ranks: sums (C, bad, flags) and extremes
+        double v[48];
+        for (int i = 0; i < 36; ++i) v[i] = st.Csum[i];
+        v[36] = st.bad;
+        v[37] = (any & AM_VOXEL_NEWTON_FAILED) ? 1.0 : 0.0;
+        v[38] = (any & AM_VOXEL_SINGULAR) ? 1.0 : 0.0;
+        v[39] = (any & AM_VOXEL_NONFINITE) ? 1.0 : 0.0;
+        v[40] = st.kmin; v[41] = -st.kmax; v[42] = st.mlo; v[43] = -st.mhi;
+        AM_CUDA(cudaMemcpyAsync(h->dsmall, v, sizeof(v), cudaMemcpyHostToDevice, h->stream));
+        AM_NCCL(ncclAllReduce(h->dsmall, h->dsmall, 40, ncclDouble, ncclSum, h->comm, h->stream));
+        AM_NCCL(ncclAllReduce(h->dsmall + 40, h->dsmall + 40, 4, ncclDouble, ncclMin, h->comm, h->stream));
+        AM_CUDA(cudaMemcpyAsync(v, h->dsmall, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
+        AM_CUDA(cudaStreamSynchronize(h->stream));
+        for (int i = 0; i < 36; ++i) st.Csum[i] = v[i];
+        st.bad = v[36];
+        any = (v[37] > 0.0 ? AM_VOXEL_NEWTON_FAILED : 0u) | (v[38] > 0.0 ? AM_VOXEL_SINGULAR : 0u) |
+              (v[39] > 0.0 ? AM_VOXEL_NONFINITE : 0u);
+        st.kmin = v[40]; st.kmax = -v[41]; st.mlo = v[42]; st.mhi = -v[43];
+    }
     h->pending = true;
     if (any & AM_VOXEL_NEWTON_FAILED) return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
     if (Cbar)
-        for (int i = 0; i < 36; ++i) Cbar[i] = st.Csum[i] / (double)h->d.N;
+        for (int i = 0; i < 36; ++i) Cbar[i] = st.Csum[i] / (double)h->N;
     if (st.bad > 0.0 || (any & AM_VOXEL_NONFINITE))
         return fail(AM_ERR_NONFINITE, "tangent field contains non-finite entries");
     if (any & AM_VOXEL_SINGULAR) return fail(AM_ERR_SINGULAR, "pivot below 1e-14 * max|A| in the tangent LU");
@@ -734,64 +995,84 @@ extern "C" int am_solver_tangent_sweep(am_solver* h, double dt, double* Cbar, do
     return AM_OK;
 }
 
-// which: 0 eps, 1 eps_n, 2 sigma; host layout (6, nx, ny, nz)
-static double* field_ptr(am_solver* h, int which) {
-    return which == 0 ? h->eps : which == 1 ? h->eps_n : which == 2 ? h->sigma : nullptr;
+// ---------------------------------------------------------------- host transfer
+// which: 0 eps, 1 eps_n, 2 sigma.  Host layout (6, nx_local, ny, nz): the
+// whole grid in local mode, this rank's x-slab in nccl mode.
+static double* Slab::*field_member(int which) {
+    return which == 0 ? &Slab::eps : which == 1 ? &Slab::eps_n : which == 2 ? &Slab::sigma : nullptr;
 }
 
-extern "C" int am_solver_get_field(am_solver* h, int which, double* out) {
-    if (!h || !out || !field_ptr(h, which)) return fail(AM_ERR_ARG, "am_solver_get_field: bad arguments");
+static int field_copy(am_solver* h, int which, double* host, bool to_host) {
+    auto f = field_member(which);
+    if (!h || !host || !f) return fail(AM_ERR_ARG, "bad field arguments");
     AM_CUDA(cudaSetDevice(h->device));
     AM_CUDA(cudaStreamSynchronize(h->stream));
-    AM_CUDA(cudaMemcpy(out, field_ptr(h, which), sizeof(double) * 6 * h->d.N, cudaMemcpyDeviceToHost));
+    const int64_t nloc = (int64_t)h->slabs.size() * h->slabs[0].Nl;  // voxels held by this process
+    for (size_t i = 0; i < h->slabs.size(); ++i) {
+        Slab& s = h->slabs[i];
+        for (int c = 0; c < 6; ++c) {
+            double* hp = host + (int64_t)c * nloc + (int64_t)i * s.Nl;
+            double* dp = s.*f + (int64_t)c * s.Nl;
+            if (to_host) AM_CUDA(cudaMemcpy(hp, dp, sizeof(double) * s.Nl, cudaMemcpyDeviceToHost));
+            else AM_CUDA(cudaMemcpy(dp, hp, sizeof(double) * s.Nl, cudaMemcpyHostToDevice));
+        }
+    }
     return AM_OK;
 }
+
+extern "C" int am_solver_get_field(am_solver* h, int which, double* out) { return field_copy(h, which, out, true); }
 
 extern "C" int am_solver_set_field(am_solver* h, int which, const double* in) {
-    if (!h || !in || !field_ptr(h, which)) return fail(AM_ERR_ARG, "am_solver_set_field: bad arguments");
+    return field_copy(h, which, const_cast<double*>(in), false);
+}
+
+// per-phase state, host (count, m) in voxel order over the local slabs;
+// pending = 0 committed, 1 pending
+static int state_copy(am_solver* h, int phase, int pending, double* host, bool to_host) {
+    if (!h || phase < 0 || phase >= (int)h->slabs[0].phases.size()) return fail(AM_ERR_ARG, "bad phase");
     AM_CUDA(cudaSetDevice(h->device));
     AM_CUDA(cudaStreamSynchronize(h->stream));
-    AM_CUDA(cudaMemcpy(field_ptr(h, which), in, sizeof(double) * 6 * h->d.N, cudaMemcpyHostToDevice));
+    int64_t off = 0;
+    for (auto& s : h->slabs) {
+        const Phase& p = s.phases[phase];
+        if (p.m && p.count) {
+            std::vector<double> soa((size_t)p.m * p.count);
+            double* dp = pending ? p.a_pend : p.a_n;
+            if (to_host) {
+                AM_CUDA(cudaMemcpy(soa.data(), dp, sizeof(double) * soa.size(), cudaMemcpyDeviceToHost));
+                for (int64_t b = 0; b < p.count; ++b)
+                    for (int c = 0; c < p.m; ++c) host[(off + b) * p.m + c] = soa[(size_t)c * p.count + b];
+            } else {
+                for (int64_t b = 0; b < p.count; ++b)
+                    for (int c = 0; c < p.m; ++c) soa[(size_t)c * p.count + b] = host[(off + b) * p.m + c];
+                AM_CUDA(cudaMemcpy(dp, soa.data(), sizeof(double) * soa.size(), cudaMemcpyHostToDevice));
+            }
+        }
+        off += p.count;
+    }
     return AM_OK;
 }
 
-// per-phase state, host AoS (count, m); pending = 0 committed, 1 pending
 extern "C" int am_solver_get_state(am_solver* h, int phase, int pending, double* out) {
-    if (!h || phase < 0 || phase >= (int)h->phases.size()) return fail(AM_ERR_ARG, "bad phase");
-    const Phase& p = h->phases[phase];
-    if (!p.m || !p.count) return AM_OK;
-    std::vector<double> soa((size_t)p.m * p.count);
-    AM_CUDA(cudaSetDevice(h->device));
-    AM_CUDA(cudaStreamSynchronize(h->stream));
-    AM_CUDA(cudaMemcpy(soa.data(), pending ? p.a_pend : p.a_n, sizeof(double) * soa.size(), cudaMemcpyDeviceToHost));
-    for (int64_t b = 0; b < p.count; ++b)
-        for (int c = 0; c < p.m; ++c) out[b * p.m + c] = soa[(size_t)c * p.count + b];
-    return AM_OK;
+    return state_copy(h, phase, pending, out, true);
 }
 
 extern "C" int am_solver_set_state(am_solver* h, int phase, const double* in) {
-    if (!h || phase < 0 || phase >= (int)h->phases.size()) return fail(AM_ERR_ARG, "bad phase");
-    const Phase& p = h->phases[phase];
-    if (!p.m || !p.count) return AM_OK;
-    std::vector<double> soa((size_t)p.m * p.count);
-    for (int64_t b = 0; b < p.count; ++b)
-        for (int c = 0; c < p.m; ++c) soa[(size_t)c * p.count + b] = in[b * p.m + c];
-    AM_CUDA(cudaSetDevice(h->device));
-    AM_CUDA(cudaStreamSynchronize(h->stream));
-    AM_CUDA(cudaMemcpy(p.a_n, soa.data(), sizeof(double) * soa.size(), cudaMemcpyHostToDevice));
-    return AM_OK;
+    return state_copy(h, phase, 0, const_cast<double*>(in), false);
 }
 
 extern "C" int am_solver_phase_count(am_solver* h, int phase, int64_t* count) {
-    if (!h || phase < 0 || phase >= (int)h->phases.size()) return fail(AM_ERR_ARG, "bad phase");
-    *count = h->phases[phase].count;
+    if (!h || !count || phase < 0 || phase >= (int)h->slabs[0].phases.size()) return fail(AM_ERR_ARG, "bad phase");
+    int64_t c = 0;
+    for (auto& s : h->slabs) c += s.phases[phase].count;
+    *count = c;
     return AM_OK;
 }
 
 // Per-phase device time of solve_step iterations (CUDA events on the solver
-// stream): out[0..4] = ms in material sweeps, D2Z, Fourier kernel +
-// reduction, origin + Z2D, and the number of iterations timed.  enable:
-// 1 on (resets the accumulators), 0 off, -1 query only.
+// stream): out[0..4] = ms in material sweeps, forward FFT, Fourier kernel +
+// reduction, origin + inverse FFT, and the number of iterations timed.
+// enable: 1 on (resets the accumulators), 0 off, -1 query only.
 extern "C" int am_solver_timing(am_solver* h, int enable, double* out) {
     if (!h) return fail(AM_ERR_ARG, "null solver");
     AM_CUDA(cudaSetDevice(h->device));
@@ -822,14 +1103,15 @@ extern "C" int am_solver_stream(am_solver* h, void** stream) {
 // GreenOperator(dims, ref).apply(tau) (homogenize.py:229-233), host (6,nx,ny,nz)
 extern "C" int am_green_apply_host(int nx, int ny, int nz, double lam, double mu, const double* tau, double* out) {
     if (nx <= 0 || ny <= 0 || nz <= 0 || !tau || !out) return fail(AM_ERR_ARG, "am_green_apply_host: bad arguments");
-    const int64_t N = (int64_t)nx * ny * nz, Nh = (int64_t)nx * ny * (nz / 2 + 1);
+    const Spec sp = spec_single(nx, ny, nz);
+    const int64_t N = sp.N, Nh = sp.cs;
     double* f = nullptr;
-    cufftDoubleComplex* c = nullptr;
+    double2* c = nullptr;
     cufftHandle p1 = 0, p2 = 0;
     int rc = AM_OK;
     long long n3[3] = {nx, ny, nz};
     size_t ws;
-    if (cudaMalloc(&f, sizeof(double) * 6 * N) != cudaSuccess || cudaMalloc(&c, sizeof(cufftDoubleComplex) * 6 * Nh) != cudaSuccess)
+    if (cudaMalloc(&f, sizeof(double) * 6 * N) != cudaSuccess || cudaMalloc(&c, sizeof(double2) * 6 * Nh) != cudaSuccess)
         rc = fail(AM_ERR_CUDA, "am_green_apply_host: out of memory");
     if (rc == AM_OK && (cufftCreate(&p1) != CUFFT_SUCCESS || cufftCreate(&p2) != CUFFT_SUCCESS ||
                         cufftMakePlanMany64(p1, 3, n3, nullptr, 1, N, nullptr, 1, Nh, CUFFT_D2Z, 6, &ws) != CUFFT_SUCCESS ||
@@ -839,8 +1121,7 @@ extern "C" int am_green_apply_host(int nx, int ny, int nz, double lam, double mu
         rc = fail(AM_ERR_CUDA, "copy failed");
     if (rc == AM_OK && cufftExecD2Z(p1, f, c) != CUFFT_SUCCESS) rc = fail(AM_ERR_CUDA, "D2Z failed");
     if (rc == AM_OK) {
-        Dims d{nx, ny, nz, nz / 2 + 1, N, Nh};
-        k_green<<<grid_for(Nh), 256>>>(d, RefMat::make(lam, mu), c);
+        k_green<<<grid_for(Nh), 256>>>(sp, RefMat::make(lam, mu), c);
         if (cudaGetLastError() != cudaSuccess) rc = fail(AM_ERR_CUDA, "k_green launch failed");
     }
     if (rc == AM_OK && cufftExecZ2D(p2, c, f) != CUFFT_SUCCESS) rc = fail(AM_ERR_CUDA, "Z2D failed");
@@ -856,16 +1137,17 @@ extern "C" int am_green_apply_host(int nx, int ny, int nz, double lam, double mu
 // equilibrium_residual(sig) (homogenize.py:241-267), host (6,nx,ny,nz)
 extern "C" int am_equilibrium_residual_host(int nx, int ny, int nz, const double* sig, double* res) {
     if (nx <= 0 || ny <= 0 || nz <= 0 || !sig || !res) return fail(AM_ERR_ARG, "bad arguments");
-    const int64_t N = (int64_t)nx * ny * nz, Nh = (int64_t)nx * ny * (nz / 2 + 1);
-    double *f = nullptr, *part = nullptr, *small = nullptr;
-    cufftDoubleComplex* c = nullptr;
+    const Spec sp = spec_single(nx, ny, nz);
+    const int64_t N = sp.N, Nh = sp.cs, L = (int64_t)ny * kParts + 8;
+    double *f = nullptr, *red = nullptr;
+    double2* c = nullptr;
     cufftHandle p1 = 0;
     int rc = AM_OK;
     long long n3[3] = {nx, ny, nz};
     size_t ws;
-    if (cudaMalloc(&f, sizeof(double) * 6 * N) != cudaSuccess ||
-        cudaMalloc(&c, sizeof(cufftDoubleComplex) * 6 * Nh) != cudaSuccess ||
-        cudaMalloc(&part, sizeof(double) * kRedBlocks) != cudaSuccess || cudaMalloc(&small, sizeof(double) * 8) != cudaSuccess)
+    std::vector<double> o(L);
+    if (cudaMalloc(&f, sizeof(double) * 6 * N) != cudaSuccess || cudaMalloc(&c, sizeof(double2) * 6 * Nh) != cudaSuccess ||
+        cudaMalloc(&red, sizeof(double) * L) != cudaSuccess)
         rc = fail(AM_ERR_CUDA, "out of memory");
     if (rc == AM_OK && (cufftCreate(&p1) != CUFFT_SUCCESS ||
                         cufftMakePlanMany64(p1, 3, n3, nullptr, 1, N, nullptr, 1, Nh, CUFFT_D2Z, 6, &ws) != CUFFT_SUCCESS))
@@ -873,21 +1155,22 @@ extern "C" int am_equilibrium_residual_host(int nx, int ny, int nz, const double
     if (rc == AM_OK && cudaMemcpy(f, sig, sizeof(double) * 6 * N, cudaMemcpyHostToDevice) != cudaSuccess)
         rc = fail(AM_ERR_CUDA, "copy failed");
     if (rc == AM_OK && cufftExecD2Z(p1, f, c) != CUFFT_SUCCESS) rc = fail(AM_ERR_CUDA, "D2Z failed");
-    double o[8];
     if (rc == AM_OK) {
-        Dims d{nx, ny, nz, nz / 2 + 1, N, Nh};
-        k_fourier<<<kRedBlocks, kRedThreads>>>(d, RefMat::make(1.0, 1.0), c, nullptr, part, 0);
-        k_finish<<<1, 1024>>>(part, kRedBlocks, c, Nh, nullptr, small);
-        if (cudaMemcpy(o, small, sizeof(o), cudaMemcpyDeviceToHost) != cudaSuccess) rc = fail(AM_ERR_CUDA, "failed");
+        k_fourier<<<ny * kParts, kRedThreads>>>(sp, RefMat::make(1.0, 1.0), c, nullptr, red, 0);
+        k_finish<<<1, 32>>>(c, sp.cs, 1, nullptr, red, (int64_t)ny * kParts);
+        if (cudaMemcpy(o.data(), red, sizeof(double) * L, cudaMemcpyDeviceToHost) != cudaSuccess)
+            rc = fail(AM_ERR_CUDA, "residual kernel failed");
     }
     if (rc == AM_OK) {
-        // the reference's sigma_bar is the voxel mean; rfft(sigma)(0) / N
+        double fsum = 0.0;
+        for (int64_t i = 0; i < (int64_t)ny * kParts; ++i) fsum += o[i];
+        // the reference's sigma_bar is the voxel mean: rfft(sigma)(0) / N
         double sbar[6];
-        for (int i = 0; i < 6; ++i) sbar[i] = o[1 + i] / (double)N;
-        *res = std::sqrt(o[0] / ((double)N * (double)N)) / std::max(dup_norm(sbar), 1e-300);
+        for (int i = 0; i < 6; ++i) sbar[i] = o[(int64_t)ny * kParts + i] / (double)N;
+        *res = std::sqrt(fsum / ((double)N * (double)N)) / std::max(dup_norm(sbar), 1e-300);
     }
     if (p1) cufftDestroy(p1);
-    cudaFree(f); cudaFree(c); cudaFree(part); cudaFree(small);
+    cudaFree(f); cudaFree(c); cudaFree(red);
     return rc;
 }
 

@@ -1,0 +1,49 @@
+"""Multi-GPU plumbing: one process per GPU, NCCL over NVLink / NVSwitch.
+
+The basic scheme's slab decomposition (csrc/solver.cu, nccl mode) needs one
+NCCL communicator shared by the ranks; torch.distributed (any backend) is
+only used to hand rank 0's NCCL unique id to the other ranks.  The material
+points (config 2) need no communicator at all: every rank evaluates its own
+batch.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class Comm:
+    """Rank, world size and the NCCL unique id of a communicator to create."""
+
+    rank: int
+    world: int
+    uid: bytes
+
+
+def nccl_unique_id():
+    """A fresh ncclUniqueId (128 bytes) from libautomat's NCCL."""
+    lib = _lib.load(require_device=False)
+    buf = ctypes.create_string_buffer(128)
+    _lib.check(lib.am_nccl_unique_id(buf), "nccl_unique_id")
+    return buf.raw
+
+
+def comm_from_torch(group=None):
+    """Build a Comm over an initialised torch.distributed process group:
+    rank 0 creates the NCCL id, the group broadcasts it."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return Comm(rank=rank, world=world, uid=obj[0])
+
+
+def slab_range(n, world, rank):
+    """x planes [x0, x0 + n/world) owned by `rank` (the decomposition of solver.cu)."""
+    if n % world:
+        raise ValueError(f"{world} ranks must divide the grid size {n}")
+    w = n // world
+    return rank * w, (rank + 1) * w

@@ -262,10 +262,16 @@ class Homogenizer:
     copies.
     """
 
-    def __init__(self, grid, cfg, threads=1, tol=1e-5, max_iterations=5000):
+    def __init__(self, grid, cfg, threads=1, tol=1e-5, max_iterations=5000, slabs=1, comm=None):
+        """``slabs`` > 1 runs the multi-GPU slab algorithm from this process on
+        one device (x-slabs, all-to-all transposes as device copies); ``comm``
+        (distributed.Comm) makes this process one rank of an NCCL-connected
+        slab decomposition, in which case host fields are the rank's x-slab
+        (6, nx / world, ny, nz) and ``grid.state`` is not synchronised."""
         from .evaluator import _validate_for_law
 
         self.grid = grid
+        self.comm = comm
         self.cfg = cfg
         self.threads = threads
         self.tol = tol
@@ -277,14 +283,24 @@ class Homogenizer:
         self._cfg = _lib.make_cfg(cfg)
         ids = np.ascontiguousarray(grid.material_ids, dtype=np.uint8)
         h = ctypes.c_void_p()
-        _lib.check(self._lib.am_solver_create(*grid.dims, _lib.ptr(ids, _lib._u8p), len(grid.materials), laws,
-                                              ctypes.byref(self._cfg), ctypes.byref(h)), "Homogenizer")
+        args = (*grid.dims, _lib.ptr(ids, _lib._u8p), len(grid.materials), laws, ctypes.byref(self._cfg))
+        if comm is not None:
+            rc = self._lib.am_solver_create_nccl(*args, comm.uid, comm.rank, comm.world, ctypes.byref(h))
+            self._local_dims = (grid.dims[0] // comm.world,) + tuple(grid.dims[1:])
+        elif slabs > 1:
+            rc = self._lib.am_solver_create_slabs(*args, int(slabs), ctypes.byref(h))
+            self._local_dims = tuple(grid.dims)
+        else:
+            rc = self._lib.am_solver_create(*args, ctypes.byref(h))
+            self._local_dims = tuple(grid.dims)
+        _lib.check(rc, "Homogenizer")
         self._h = h
         self._ebar_n = np.zeros(6)
         self._last = None  # (eps, ebar) host arrays of the last converged step
         self._pending = False
-        self._push_state(grid._state)
-        grid._solver = self
+        if comm is None:
+            self._push_state(grid._state)
+            grid._solver = self
         self.reference = None
         self.set_reference(self.elastic_reference())
 
@@ -310,12 +326,14 @@ class Homogenizer:
                 arr[:] = buf
 
     def _get(self, which):
-        out = np.empty((6,) + tuple(self.grid.dims))
+        out = np.empty((6,) + self._local_dims)
         _lib.check(self._lib.am_solver_get_field(self._h, which, _lib.ptr(out)))
         return out
 
     def _set(self, which, field):
         f = _field(field)
+        if f.shape[1:] != self._local_dims:
+            raise ValueError(f"field dims {f.shape[1:]} != {self._local_dims}")
         _lib.check(self._lib.am_solver_set_field(self._h, which, _lib.ptr(f)))
 
     @property
@@ -425,13 +443,15 @@ class Homogenizer:
         self._last = None
 
 
-def run_loading_path(grid, path, cfg, update_reference=True, threads=1, tol=1e-5, max_iterations=5000):
+def run_loading_path(grid, path, cfg, update_reference=True, threads=1, tol=1e-5, max_iterations=5000, slabs=1,
+                     comm=None):
     """March the loading path; one record dict per step (homogenize.py:485-528).
 
     Device-resident: per step the basic scheme, then (update_reference) the
     tangent sweep fused with reference_update, commit, new reference.
+    ``slabs`` / ``comm``: see Homogenizer (every rank returns the same records).
     """
-    hom = Homogenizer(grid, cfg, threads=threads, tol=tol, max_iterations=max_iterations)
+    hom = Homogenizer(grid, cfg, threads=threads, tol=tol, max_iterations=max_iterations, slabs=slabs, comm=comm)
     lib = hom._lib
     times = path.times()
     eps_targets = path.eps_xx(times)
@@ -458,6 +478,8 @@ def run_loading_path(grid, path, cfg, update_reference=True, threads=1, tol=1e-5
             hom._ebar_n = ebar
             _lib.check(lib.am_solver_commit(hom._h, _lib.ptr(ebar)))
         hom._pending = False
+        if k == len(times) - 1 and comm is None:
+            hom.grid.state  # noqa: B018  (refresh the host copy of the final state)
         records.append({
             "step": k, "time": float(times[k]), "eps_xx": float(ebar[0]), "sig": sig_bar.copy(),
             "C11": C11, "C12": C12, "iterations": info.iterations, "mean_substeps": info.mean_substeps,
