@@ -156,19 +156,24 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def basic_scheme(n, lib, dev):
+def basic_scheme(n, lib, dev, dist=None):
     """Basic-scheme iterations/s on config 4's microstructure (toy_mmc_grid(n),
     elasto-viscoplastic matrix + elastic fibre), load step 1 of
     LoadingPath(steps=20) with mixed BCs, device-resident; per-phase times
-    from am_solver_timing (CUDA events on the solver stream)."""
+    from am_solver_timing (CUDA events on the solver stream).  Under torchrun
+    the grid is x-slab decomposed over the ranks (NCCL all-to-all transposes,
+    strong scaling); the time is the max over ranks."""
     import torch
+
+    from paper_2006_04391_b200 import distributed as D
 
     from paper_2006_04391_b200 import _lib, homogenize as H
     from paper_2006_04391_b200.evaluator import StrategyConfig
 
     cfg = StrategyConfig(strategy="automatic", integrator="implicit-euler")
     grid = H.toy_mmc_grid(n)
-    hom = H.Homogenizer(grid, cfg)
+    comm = D.comm_from_torch() if dist is not None else None
+    hom = H.Homogenizer(grid, cfg, comm=comm)
     sp = ctypes.c_void_p()
     _lib.check(lib.am_solver_stream(hom._h, ctypes.byref(sp)))
     stream = torch.cuda.ExternalStream(sp.value, device=dev)
@@ -186,18 +191,25 @@ def basic_scheme(n, lib, dev):
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     ph = np.zeros(5)
     _lib.check(lib.am_solver_timing(hom._h, -1, _lib.ptr(ph)))
     iters = info.iterations
     N = n ** 3
-    Nh = n * n * (n // 2 + 1)
+    world = comm.world if comm is not None else 1
+    Nh = n * n * (n // 2 + 1) // world  # rfft bins per rank
     it_t = ph[4] or 1.0
     fourier_ms = ph[2] / it_t
     fourier_bytes = 4 * 96.0 * Nh  # read shat, ehat; write ehat, shat (complex128 x 6)
     return {
         "metric": "basic-scheme iterations/s", "value": iters / (ms * 1e-3), "unit": "it/s",
         "config": {"workload": f"config 4 grid toy_mmc_grid({n}) (EVP matrix, VF 0.10 elastic fibre), "
-                               "load step 1 of LoadingPath(steps=20), mixed BC, tol 1e-5, 1 GPU",
+                               f"load step 1 of LoadingPath(steps=20), mixed BC, tol 1e-5, {world} GPU(s)",
+                   "parallelism": "single GPU (3-D cuFFT)" if world == 1 else
+                   f"x-slabs over {world} GPUs, NCCL all-to-all transposes (strong scaling)",
                    "voxels": N, "evp_voxels": int(len(grid.voxel_index[0]))},
         "iterations": iters, "ms_total": ms, "ms_per_iteration": ms / iters,
         "phase_ms_per_iteration": {"material": ph[0] / it_t, "d2z": ph[1] / it_t, "fourier+reduce": fourier_ms,
@@ -340,6 +352,8 @@ def main():
     assert np.array_equal(h_it, iters), "e2e path disagrees with the device path"
     h2d = B * (6 + 7 + 6 + 1) * 8
     d2h = B * (6 + 7 + 36) * 8 + B * 4
+    clocks = clk.summary()
+    basic = basic_scheme(args.basic, lib, dev, dist) if args.basic else None
 
     if rank != 0:
         if dist is not None:
@@ -364,10 +378,10 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "am_eval_batch_host (C ABI), pinned host AoS buffers, 2-stream chunked H2D|kernel|D2H"},
         "gpu_launches": 2 * args.steps,
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
-    if args.basic:
-        line["basic_scheme"] = basic_scheme(args.basic, lib, dev)
+    if basic is not None:
+        line["basic_scheme"] = basic
         line["gpu_launches_note"] = "gpu_launches counts the config-2 K1 launches of the timed region"
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
