@@ -236,6 +236,34 @@ AM_HD double rms(const double* x) {
     return sqrt(s / N);
 }
 
+// mean square (the square of rms without the sqrt and the division; used
+// for comparisons, which sqrt preserves)
+template <int N>
+AM_HD double msq(const double* x) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) s += x[i] * x[i];
+    return s * (1.0 / N);
+}
+
+// reciprocal for finite nonzero y: hardware approximation + two
+// Newton-Raphson steps (within an ulp of 1/y; the IEEE division costs an
+// extra multiply-correct sequence and a slow-path branch).  Non-finite or
+// zero y give NaN / inf; callers only use it where those cases are already
+// flagged by other tests.
+AM_HD double frcp(double y) {
+#ifdef __CUDA_ARCH__
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+    double e = fma(-y, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-y, r, 1.0);
+    return fma(r, e, r);
+#else
+    return 1.0 / y;
+#endif
+}
+
 
 #ifdef __CUDACC__
 #define AM_COLD __host__ __device__ __noinline__
@@ -315,7 +343,7 @@ struct SFact {
         for (int k = 0; k < nd; ++k) {
             const double p = D[k][k];
             ok = ok && (fabs(p) >= 1e-9 * dsum);
-            const double iv = 1.0 / p;
+            const double iv = frcp(p);
             inv[k] = iv;
 #pragma unroll
             for (int i = k + 1; i < nd; ++i) {
@@ -503,6 +531,7 @@ AM_HD int newton_point(const Law& L, const NewtonCfg& cfg, const double* eps_n, 
         step_strain(eps_n, eps_np1, dt, e1);
         double res_prev = INFINITY;
         int growth = 0;
+        const double tol2 = cfg.tol * cfg.tol;
         double sig_prev[6];
         if constexpr (Mode == 1) stress_plain(L, e1, a, sig_prev);
         for (;;) {
@@ -534,9 +563,10 @@ AM_HD int newton_point(const Law& L, const NewtonCfg& cfg, const double* eps_n, 
 #pragma unroll
             for (int i = 0; i < m; ++i) {
                 an[i] = a[i] - dl[i];
-                sc[i] = F[i] / (1.0 + fabs(a[i]));
+                sc[i] = F[i] * frcp(1.0 + fabs(a[i]));
             }
-            const double res = rms<m>(sc);
+            // residual RMS (odeint.py:384); compared in squares (sqrt is monotone)
+            const double res = msq<m>(sc);
             growth = res > res_prev ? growth + 1 : 0;
             res_prev = res;
             bool conv;
@@ -551,8 +581,8 @@ AM_HD int newton_point(const Law& L, const NewtonCfg& cfg, const double* eps_n, 
                 for (int i = 0; i < 6; ++i) sig_prev[i] = sn[i];
             } else {
 #pragma unroll
-                for (int i = 0; i < m; ++i) sc[i] = dl[i] / (1.0 + fabs(an[i]));
-                conv = rms<m>(sc) <= cfg.tol;
+                for (int i = 0; i < m; ++i) sc[i] = dl[i] * frcp(1.0 + fabs(an[i]));
+                conv = msq<m>(sc) <= tol2;  // rms <= tol (odeint.py:395)
             }
 #pragma unroll
             for (int i = 0; i < m; ++i) a[i] = an[i];
