@@ -189,15 +189,25 @@ AM_HD D<A> dpow(const D<A>& x, double c) {
 }
 // Value and local partial of a constant-exponent power node as duals:
 // val = x^c (dual), dval = c * x^(c-1) (dual, i.e. including c(c-1)x^(c-2)dx).
-// One pow(x, c-2) yields all three powers (x^(c-1) = x^(c-2)*x, x^c =
+// One x^(c-2) yields all three powers (x^(c-1) = x^(c-2)*x, x^c =
 // x^(c-1)*x) whenever that is exact in the limit: x > 0, or c >= 2 (x = 0
 // gives 0^(c-2) in {0, 1} and zero higher powers).  Otherwise the powers are
-// taken separately like Dual1.__pow__ (ad.py:99-100).  Relative difference
-// to separate pow() calls: a few ulp.
+// taken separately like Dual1.__pow__ (ad.py:99-100).
 template <uint32_t A>
 AM_HD void powjet(const D<A>& x, double c, D<A>& val, D<A>& dval) {
     double p0, p1, p2;
-    if (x.v > 0.0 || c >= 2.0) {
+    if (x.v > 0.0) {
+#ifdef AM_EXACT_POW
+        p2 = ::pow(x.v, c - 2.0);
+#else
+        // exp((c-2) log x): a third of pow()'s instructions (pow evaluates
+        // the logarithm in double-double); relative error ~|c ln x| ulp,
+        // i.e. <= 1e-14 for the overstress ratios of the Norton law
+        p2 = ::exp((c - 2.0) * ::log(x.v));
+#endif
+        p1 = p2 * x.v;
+        p0 = p1 * x.v;
+    } else if (c >= 2.0) {
         p2 = ::pow(x.v, c - 2.0);
         p1 = p2 * x.v;
         p0 = p1 * x.v;

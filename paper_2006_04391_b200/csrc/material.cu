@@ -11,6 +11,7 @@
 // stride, item stride) pairs so the same kernel serves SoA device fields
 // (coalesced: consecutive threads touch consecutive doubles) and the
 // reference's AoS host layout on the host-pointer path.
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -42,11 +43,11 @@ struct GlobalSink {
 //   k_tangent<Law>              tangent post-process + clamp + stress + C.
 // Mode = Newton convergence measure; each combination is its own
 // instantiation so the hot Newton loop carries no dead code
-// (instruction-cache footprint).  The Newton kernel runs best at 4 CTAs per
-// SM (128 registers), the tangent kernel with the full 255-register budget
+// (instruction-cache footprint).  The Newton kernel runs best at 3 CTAs per
+// SM (168 registers), the tangent kernel with the full 255-register budget
 // (tools/k1_variants.py measurements).
 #ifndef AM_K1_MINB_N
-#define AM_K1_MINB_N 4
+#define AM_K1_MINB_N 3
 #endif
 #ifndef AM_K1_MINB_T
 #define AM_K1_MINB_T 1
@@ -189,6 +190,24 @@ int check_cfg(const am_cfg* cfg) {
 
 NewtonCfg newton_cfg(const am_cfg* cfg) { return NewtonCfg{cfg->newton_mode, cfg->max_newton, cfg->newton_tol}; }
 
+// Stream-ordered scratch comes from the device's default memory pool; keep
+// freed blocks in the pool (release threshold = max) so per-call
+// allocations do not return memory to the driver at every synchronisation.
+static void keep_pool_memory() {
+    static std::mutex mu;
+    static std::vector<int> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~uint64_t(0);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done.push_back(dev);
+}
+
 template <class Law>
 static int launch_law(const Law& L, KArgs k, cudaStream_t s) {
     const int threads = 128;
@@ -207,6 +226,7 @@ static int launch_law(const Law& L, KArgs k, cudaStream_t s) {
     // does not want it)
     uint8_t* scratch = nullptr;
     if (Law::m > 0 && !k.status) {
+        keep_pool_memory();
         AM_CUDA(cudaMallocAsync((void**)&scratch, (size_t)k.B, s));
         k.status = scratch;
     }
