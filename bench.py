@@ -323,6 +323,12 @@ def main():
     iters = d_it.cpu().numpy()
     fl = float(np.sum(flops_per_eval(iters.astype(np.float64))))
     achieved = fl / (ms * 1e-3) / 1e12
+    traffic = None
+    try:  # DRAM bytes per point of the two K1 kernels from the committed ncu capture
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
+        traffic = B * (tj["k_material_newton_raw_bytes_per_point"] + tj["k_tangent_bytes_per_point"])
+    except (OSError, KeyError, ValueError):
+        pass
     peak = ctypes.c_double(0.0)
     _lib.check(lib.am_probe_fp64_tflops(5, ctypes.byref(peak)))
 
@@ -370,7 +376,8 @@ def main():
                    "l2": "inputs+outputs 552 MiB per step > 126 MB L2 (no flush needed)",
                    "mean_newton_iters": float(iters.mean())},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                     "frac": achieved / peak.value if peak.value else None, "traffic": None,
+                     "frac": achieved / peak.value if peak.value else None, "traffic": traffic,
+                     "traffic_source": "ncu dram bytes per point (profiles/r01/traffic.json) x points per step",
                      "peak_source": "measured: am_probe_fp64_tflops DFMA microbenchmark on this GPU "
                                     "(MEASURED_PEAKS.json has no fp64 entry)",
                      "work_per_launch": f"{fl:.4g} algorithmic fp64 flops per step (SURVEY §8d: 1072*N_it + 2273 per eval); "
