@@ -223,6 +223,32 @@ def basic_scheme(n, lib, dev, dist=None):
     }
 
 
+def loading_path_bench(n, dev, dist=None, steps=20):
+    """Config 3: the full 20-step loading path (tension-compression, mixed BC,
+    reference update every step) on toy_mmc_grid(n) through the public
+    run_loading_path, device time on the solver stream via am_solver_timing
+    plus wall time of the whole call (tangent sweeps included)."""
+    import torch
+
+    from paper_2006_04391_b200 import distributed as D, homogenize as H
+    from paper_2006_04391_b200.evaluator import StrategyConfig
+
+    cfg = StrategyConfig(strategy="automatic", integrator="implicit-euler")
+    grid = H.toy_mmc_grid(n)
+    comm = D.comm_from_torch() if dist is not None else None
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    recs = H.run_loading_path(grid, H.LoadingPath(steps=steps), cfg, comm=comm)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    its = int(sum(r["iterations"] for r in recs))
+    return {"metric": "basic-scheme iterations/s over the loading path", "value": its / wall, "unit": "it/s",
+            "config": {"workload": f"config 3: toy_mmc_grid({n}), LoadingPath(steps={steps}), mixed BC, "
+                                   "reference update per step, run_loading_path (wall clock incl. tangent sweeps)"},
+            "seconds": wall, "iterations_total": its, "iterations_per_step": [r["iterations"] for r in recs],
+            "sig_xx_final": float(recs[-1]["sig"][0]), "C11_final": recs[-1]["C11"]}
+
+
 def hbm_peak():
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -239,6 +265,7 @@ def main():
     ap.add_argument("--batch", type=int, default=B_DEFAULT)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--basic", type=int, default=256, help="grid size n of the basic-scheme line (0: skip)")
+    ap.add_argument("--path", type=int, default=128, help="grid size n of the config-3 loading path (0: skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -287,7 +314,7 @@ def main():
 
     def step():
         rc = lib.am_eval_batch(s_law, s_cfg, B, d_en.data_ptr(), d_an.data_ptr(), d_ep.data_ptr(), d_dt.data_ptr(),
-                               0.0, 1, d_sig.data_ptr(), d_a.data_ptr(), d_C.data_ptr(), d_it.data_ptr(),
+                               0.0, 1, d_sig.data_ptr(), d_a.data_ptr(), d_C.data_ptr(), d_it.data_ptr(), None,
                                d_st.data_ptr(), d_fl.data_ptr(), sp)
         if rc:
             _lib.check(rc)
@@ -340,7 +367,8 @@ def main():
 
     def e2e_step():
         rc = lib.am_eval_batch_host(s_law, s_cfg, B, _lib.ptr(h_en), _lib.ptr(h_an), _lib.ptr(h_ep), _lib.ptr(h_dt),
-                                    1, _lib.ptr(h_sig), _lib.ptr(h_a), _lib.ptr(h_C), _lib.ptr(h_it, _lib._i32p), None)
+                                    1, _lib.ptr(h_sig), _lib.ptr(h_a), _lib.ptr(h_C), _lib.ptr(h_it, _lib._i32p), None,
+                                    None)
         _lib.check(rc)
 
     for _ in range(2):
@@ -360,6 +388,7 @@ def main():
     d2h = B * (6 + 7 + 36) * 8 + B * 4
     clocks = clk.summary()
     basic = basic_scheme(args.basic, lib, dev, dist) if args.basic else None
+    path = loading_path_bench(args.path, dev, dist) if args.path else None
 
     if rank != 0:
         if dist is not None:
@@ -387,6 +416,8 @@ def main():
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
     }
+    if path is not None:
+        line["loading_path"] = path
     if basic is not None:
         line["basic_scheme"] = basic
         line["gpu_launches_note"] = "gpu_launches counts the config-2 K1 launches of the timed region"

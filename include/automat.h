@@ -37,13 +37,15 @@ typedef enum am_status {
     AM_ERR_CUDA = 5,
     AM_ERR_NCCL = 6,
     AM_ERR_ARG = 7,               /* ValueError on bad arguments */
-    AM_ERR_NONFINITE = 8          /* reference_update: non-finite tangent (homogenize.py:316-317) */
+    AM_ERR_NONFINITE = 8,         /* reference_update: non-finite tangent (homogenize.py:316-317) */
+    AM_ERR_INTEGRATION = 9        /* odeint.IntegrationError: substep cap / step underflow (odeint.py:30-31) */
 } am_status;
 
 /* per-voxel status bits written by the material kernel */
 #define AM_VOXEL_NEWTON_FAILED 1u
 #define AM_VOXEL_SINGULAR 2u
 #define AM_VOXEL_NONFINITE 4u
+#define AM_VOXEL_INTEGRATION 8u
 
 /* ---------------------------------------------------------------- laws
  * A law is its two potentials; the potentials live on the device.
@@ -62,8 +64,8 @@ typedef struct am_law {
 /* ---------------------------------------------------------------- config
  * StrategyConfig (evaluator.py:35-74).  Order of the enums follows
  * STRATEGIES / INTEGRATORS / ERROR_MEASURES (evaluator.py:26-28).  This
- * build implements strategy=automatic x integrator=implicit-euler; other
- * combinations return AM_ERR_CONFIG.
+ * build implements strategy=automatic with the implicit-euler, ode12 and
+ * ode23 integrators; other combinations return AM_ERR_CONFIG.
  */
 enum { AM_STRATEGY_CONVENTIONAL = 0, AM_STRATEGY_AUTOMATIC = 1, AM_STRATEGY_SEMI_AUTOMATIC = 2 };
 enum { AM_INTEGRATOR_IMPLICIT_EULER = 0, AM_INTEGRATOR_ODE12 = 1, AM_INTEGRATOR_ODE23 = 2, AM_INTEGRATOR_ODE23S = 3 };
@@ -75,6 +77,10 @@ typedef struct am_cfg {
     int32_t newton_mode;     /* resolved_newton_mode (evaluator.py:69-71) */
     int32_t max_newton;      /* 50 (odeint.py:371) */
     double newton_tol;       /* 1e-10 (odeint.py:404) */
+    /* adaptive integrators (StepController, odeint.py:198-214) */
+    int32_t error_measure;   /* 0 internal, 1 stress (evaluator.py:28) */
+    int32_t max_substeps;    /* 10000 */
+    double atol, rtol;       /* 1e-6, 1e-3 */
 } am_cfg;
 
 /* ---------------------------------------------------------------- library */
@@ -90,8 +96,11 @@ int am_set_device(int device);
  *   eps_n, eps_np1: 6*B      a_n, a_out: m*B (m = 7 Michel-Suquet, 0 elastic)
  *   dt: B values, or NULL to use dt_scalar for every item
  *   sigma: 6*B   C: 36*B (C[(i*6+j)*B + b] = dsigma_i/deps_j) or NULL
- *   newton_iters (int32, B) / status (uint8, B) / flags (one uint32 that
- *   receives the OR of all status bits): each optional (NULL).
+ *   newton_iters (int32, B): implicit Euler: the per-point Newton count;
+ *   adaptive integrators: accepted substeps (EvalResult.substeps)
+ *   rejected (int32, B): rejected attempts of the adaptive integrators (0 for
+ *   implicit Euler) / status (uint8, B) / flags (one uint32 that receives
+ *   the OR of all status bits): each optional (NULL).
  * Returns AM_OK once the work is enqueued; per-voxel failures are reported
  * through status / flags (NewtonDivergenceError / SingularMatrixError are
  * raised from them by the caller, see am_eval_batch_host).
@@ -100,7 +109,7 @@ int am_eval_batch(const am_law *law, const am_cfg *cfg, int64_t B,
                   const double *eps_n, const double *a_n, const double *eps_np1,
                   const double *dt, double dt_scalar, int want_tangent,
                   double *sigma, double *a_out, double *C,
-                  int32_t *newton_iters, uint8_t *status, uint32_t *flags, void *stream);
+                  int32_t *newton_iters, int32_t *rejected, uint8_t *status, uint32_t *flags, void *stream);
 
 /*
  * am_eval_batch_host -- same as evaluate_arrays with the reference's host
@@ -108,14 +117,15 @@ int am_eval_batch(const am_law *law, const am_cfg *cfg, int64_t B,
  * C (B,6,6) or NULL.  Pinned or pageable memory.  Synchronous.  The batch is
  * pipelined through the GPU in chunks over two streams (H2D | kernel | D2H).
  * Returns AM_ERR_NEWTON if any voxel's Newton failed (odeint.py:415-416),
- * else AM_ERR_SINGULAR if any tangent LU was singular (odeint.py:424), else
- * AM_OK.  Outputs are written for every voxel in all cases.
+ * AM_ERR_INTEGRATION if an adaptive integration hit a cap (odeint.py:
+ * 690-691, 740-744), else AM_ERR_SINGULAR if any tangent LU was singular
+ * (odeint.py:424), else AM_OK.  Outputs are written for every voxel.
  */
 int am_eval_batch_host(const am_law *law, const am_cfg *cfg, int64_t B,
                        const double *eps_n, const double *a_n, const double *eps_np1,
                        const double *dt, int want_tangent,
                        double *sigma, double *a_out, double *C,
-                       int32_t *newton_iters, uint8_t *status);
+                       int32_t *newton_iters, int32_t *rejected, uint8_t *status);
 
 /*
  * am_constitutive_host -- module-level constitutive operations at B points

@@ -23,6 +23,7 @@ AM_ERR_CUDA = 5
 AM_ERR_NCCL = 6
 AM_ERR_ARG = 7
 AM_ERR_NONFINITE = 8
+AM_ERR_INTEGRATION = 9
 
 AM_LAW_LINEAR_ELASTIC = 0
 AM_LAW_MICHEL_SUQUET = 1
@@ -33,6 +34,8 @@ NEWTON_CODES = {"internal": 0, "stress": 1}
 VOXEL_NEWTON_FAILED = 1
 VOXEL_SINGULAR = 2
 VOXEL_NONFINITE = 4
+VOXEL_INTEGRATION = 8
+ERROR_MEASURE_CODES = {"internal": 0, "stress": 1}
 
 
 class am_law(ctypes.Structure):
@@ -49,6 +52,8 @@ class am_cfg(ctypes.Structure):
         ("strategy", ctypes.c_int32), ("integrator", ctypes.c_int32),
         ("newton_mode", ctypes.c_int32), ("max_newton", ctypes.c_int32),
         ("newton_tol", ctypes.c_double),
+        ("error_measure", ctypes.c_int32), ("max_substeps", ctypes.c_int32),
+        ("atol", ctypes.c_double), ("rtol", ctypes.c_double),
     ]
 
 
@@ -77,11 +82,11 @@ SIGNATURES = {
     "am_eval_batch": (ctypes.c_int, [
         ctypes.POINTER(am_law), ctypes.POINTER(am_cfg), ctypes.c_int64,
         _vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_int,
-        _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+        _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
     ]),
     "am_eval_batch_host": (ctypes.c_int, [
         ctypes.POINTER(am_law), ctypes.POINTER(am_cfg), ctypes.c_int64,
-        _dp, _dp, _dp, _dp, ctypes.c_int, _dp, _dp, _dp, _i32p, _u8p,
+        _dp, _dp, _dp, _dp, ctypes.c_int, _dp, _dp, _dp, _i32p, _i32p, _u8p,
     ]),
     "am_probe_fp64_tflops": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "am_constitutive_host": (ctypes.c_int, [
@@ -199,6 +204,10 @@ def make_cfg(cfg):
     s.newton_mode = NEWTON_CODES[cfg.resolved_newton_mode]
     s.max_newton = 50
     s.newton_tol = 1e-10
+    s.error_measure = ERROR_MEASURE_CODES[cfg.error_measure]
+    s.max_substeps = int(cfg.max_substeps)
+    s.atol = float(cfg.atol)
+    s.rtol = float(cfg.rtol)
     return s
 
 
@@ -211,12 +220,14 @@ def check(rc, where=""):
         msg = f"{where}: {msg}"
     from .evaluator import ConfigError
     from .linalg import SingularMatrixError
-    from .odeint import NewtonDivergenceError
+    from .odeint import IntegrationError, NewtonDivergenceError
 
     if rc == AM_ERR_CONFIG:
         raise ConfigError(msg)
     if rc == AM_ERR_NEWTON:
         raise NewtonDivergenceError(msg)
+    if rc == AM_ERR_INTEGRATION:
+        raise IntegrationError(msg)
     if rc == AM_ERR_SINGULAR:
         raise SingularMatrixError(msg)
     if rc == AM_ERR_NOT_CONVERGED:

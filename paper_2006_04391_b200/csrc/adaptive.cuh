@@ -1,0 +1,270 @@
+// adaptive.cuh -- adaptive explicit embedded integration of one material
+// point (gsmkit odeint.py: ode12 / ode23 SchemeSpec 92-113, _explicit_step
+// 429-475, error_norm 564-617, adaptive_integrate 636-756, StepController
+// 198-214), automatic strategy, with optional coupled sensitivity transport
+// (Theorem 2 / Corollary 1 of the paper: the sensitivity da/deps_{n+1} is
+// advanced by the same scheme through forward-mode duals of f).
+//
+// Everything is per point: the FSAL slope reuse, the step controller and
+// the caps act on this point only, exactly as the reference's masked batch
+// code does per voxel ("a voxel's arithmetic never depends on its batch
+// company", odeint.py:432-434).  Host + device.
+#pragma once
+
+#include "material.cuh"
+
+namespace am {
+
+enum : int { ST_INTEGRATION = 8 };  // IntegrationError (odeint.py:30-31): caps / underflow
+
+// Butcher tableaux (ode12 odeint.py:92-105, ode23 odeint.py:108-128)
+template <int Scheme>
+struct Tableau;
+template <>
+struct Tableau<12> {
+    static constexpr int s = 2;
+    static constexpr bool fsal = false;
+    static constexpr int order_low = 1;
+    AM_HD static double a(int i, int j) { return (i == 1 && j == 0) ? 1.0 : 0.0; }
+    AM_HD static double b(int j) { return 0.5; }
+    AM_HD static double be(int j) { return j == 0 ? 1.0 : 0.0; }
+    AM_HD static double c(int i) { return i == 1 ? 1.0 : 0.0; }
+};
+template <>
+struct Tableau<23> {
+    static constexpr int s = 4;
+    static constexpr bool fsal = true;
+    static constexpr int order_low = 2;
+    AM_HD static double a(int i, int j) {
+        if (i == 1) return j == 0 ? 0.5 : 0.0;
+        if (i == 2) return j == 1 ? 0.75 : 0.0;
+        if (i == 3) return j == 0 ? 2.0 / 9.0 : (j == 1 ? 1.0 / 3.0 : (j == 2 ? 4.0 / 9.0 : 0.0));
+        return 0.0;
+    }
+    AM_HD static double b(int j) { return j == 0 ? 2.0 / 9.0 : (j == 1 ? 1.0 / 3.0 : (j == 2 ? 4.0 / 9.0 : 0.0)); }
+    AM_HD static double be(int j) { return j == 0 ? 7.0 / 24.0 : (j == 1 ? 0.25 : (j == 2 ? 1.0 / 3.0 : 0.125)); }
+    // row sums of a (SchemeSpec.c)
+    AM_HD static double c(int i) { return i == 0 ? 0.0 : (i == 1 ? 0.5 : (i == 2 ? 0.75 : 1.0)); }
+};
+
+// strain at time t of the step and its ramp r = min(t/dt, 1) (odeint.py:256-264)
+AM_HD double strain_at(const double* eps_n, const double* eps_np1, double t, double dt, double* e) {
+    double r = t / dt;
+    r = r < 1.0 ? r : 1.0;
+    for (int i = 0; i < 6; ++i) e[i] = eps_n[i] + r * (eps_np1[i] - eps_n[i]);
+    return r;
+}
+
+// MaterialStepProblem.rhs (odeint.py:286-288)
+template <class Law>
+AM_HD void rhs_plain(const Law& L, const double* e, const double* a, double* f) {
+    auto fv = rhs_sweep(L, plain_tup<6>(e, seq<6>{}), plain_tup<Law::m>(a, seq<Law::m>{}));
+    sfor<Law::m>([&](auto I) { f[decltype(I)::value] = get<decltype(I)::value>(fv).v; });
+}
+
+template <int... I>
+AM_HD auto dual6_tup(const double* a, const double (*da)[6], std::integer_sequence<int, I...>) {
+    auto mk = [&](int k) {
+        D<0x3Fu> p;
+        p.v = a[k];
+        for (int j = 0; j < 6; ++j) p.d[j] = da[k][j];
+        return p;
+    };
+    return tup(mk(I)...);
+}
+
+// MaterialStepProblem.rhs_dual (odeint.py:298-304): f and
+// df/da . ydot + df/deps_{n+1} with eps(t) seeded r * I
+template <class Law>
+AM_HD void rhs_dual_pt(const Law& L, const double* e, double r, const double* a, const double (*ad)[6], double* f,
+                       double (*fd)[6]) {
+    auto fv = rhs_sweep(L, seed_tup<0>(e, r, seq<6>{}), dual6_tup(a, ad, seq<Law::m>{}));
+    sfor<Law::m>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        f[i] = get<i>(fv).v;
+        sfor<6>([&](auto K) { fd[i][decltype(K)::value] = get<i>(fv).template dir<decltype(K)::value>(); });
+    });
+}
+
+// MaterialStepProblem.stress_of / stress_dual (odeint.py:339-352)
+template <class Law>
+AM_HD void stress_dual_pt(const Law& L, const double* e, double r, const double* a, const double (*ad)[6],
+                          double* sig, double (*C)[6]) {
+    auto s = stress_sweep(L, seed_tup<0>(e, r, seq<6>{}), dual6_tup(a, ad, seq<Law::m>{}));
+    sfor<6>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        sig[i] = get<i>(s).v;
+        sfor<6>([&](auto K) { C[i][decltype(K)::value] = get<i>(s).template dir<decltype(K)::value>(); });
+    });
+}
+
+// _scaled_sq (odeint.py:559-561) accumulated
+AM_HD double scaled_sq(double diff, double ra, double rb, double atol, double rtol) {
+    const double sc = atol + rtol * fmax(fabs(ra), fabs(rb));
+    const double x = diff / sc;
+    return x * x;
+}
+
+// One point over [0, dt] (adaptive_integrate, odeint.py:636-756).  Writes the
+// unclamped state to a and (Coupled) da = da/deps_{n+1}; substeps / rejected
+// counts.  Returns status bits (ST_INTEGRATION when a cap or the step-size
+// underflow would raise IntegrationError).
+template <class Law, int Scheme, bool Coupled>
+AM_HD int adaptive_point(const Law& L, const StepCtl& ctl, const double* eps_n, const double* a_n,
+                         const double* eps_np1, double dt, double* a, double (*da)[6], int& substeps, int& rejected) {
+    using T = Tableau<Scheme>;
+    constexpr int m = Law::m;
+    constexpr int s = T::s;
+    for (int i = 0; i < m; ++i) {
+        a[i] = a_n[i];
+        if (Coupled)
+            for (int j = 0; j < 6; ++j) da[i][j] = 0.0;
+    }
+    substeps = rejected = 0;
+    double t = 0.0, h = dt;
+    bool accepted_any = false, g1_valid = false;
+    double g1[m], gd1[Coupled ? m : 1][6];
+    const int max_attempts = ctl.max_substeps * 4;
+    for (int attempts = 1;; ++attempts) {
+        if (attempts > max_attempts) return ST_INTEGRATION;  // global attempt cap
+        double hi = fmin(h, dt - t);
+        const bool clipped = hi >= dt - t - 1e-15 * dt;
+        double G[s][m], Gd[Coupled ? s : 1][Coupled ? m : 1][6];
+        double yi[m], ydi[Coupled ? m : 1][6];
+        for (int st = 0; st < s; ++st) {
+            if (st == 0 && g1_valid) {  // FSAL reuse (odeint.py:443-453)
+                for (int i = 0; i < m; ++i) {
+                    G[0][i] = g1[i];
+                    if (Coupled)
+                        for (int j = 0; j < 6; ++j) Gd[0][i][j] = gd1[i][j];
+                }
+                continue;
+            }
+            for (int i = 0; i < m; ++i) {
+                yi[i] = a[i];
+                if (Coupled)
+                    for (int j = 0; j < 6; ++j) ydi[i][j] = da[i][j];
+            }
+            for (int q = 0; q < st; ++q) {
+                const double aq = T::a(st, q);
+                if (aq == 0.0) continue;
+                const double w = hi * aq;
+                for (int i = 0; i < m; ++i) {
+                    yi[i] += w * G[q][i];
+                    if (Coupled)
+                        for (int j = 0; j < 6; ++j) ydi[i][j] += w * Gd[q][i][j];
+                }
+            }
+            const double ti = t + T::c(st) * hi;
+            double e[6];
+            const double r = strain_at(eps_n, eps_np1, ti, dt, e);
+            if constexpr (Coupled) rhs_dual_pt(L, e, r, yi, ydi, G[st], Gd[st]);
+            else rhs_plain(L, e, yi, G[st]);
+        }
+        double yh[m], yl[m], dh[Coupled ? m : 1][6], dl[Coupled ? m : 1][6];
+        bool ok = true;
+        for (int i = 0; i < m; ++i) {
+            double sh = 0.0, sl = 0.0;
+            for (int q = 0; q < s; ++q) {
+                sh += T::b(q) * G[q][i];
+                sl += T::be(q) * G[q][i];
+            }
+            yh[i] = a[i] + hi * sh;
+            yl[i] = a[i] + hi * sl;
+            ok = ok && (yh[i] - yh[i] == 0.0) && (yl[i] - yl[i] == 0.0);
+            if (Coupled)
+                for (int j = 0; j < 6; ++j) {
+                    double ch = 0.0, cl = 0.0;
+                    for (int q = 0; q < s; ++q) {
+                        ch += T::b(q) * Gd[q][i][j];
+                        cl += T::be(q) * Gd[q][i][j];
+                    }
+                    dh[i][j] = da[i][j] + hi * ch;
+                    dl[i][j] = da[i][j] + hi * cl;
+                }
+        }
+        // error_norm (odeint.py:564-617)
+        double total = 0.0;
+        int count;
+        if (ctl.measure == 0) {
+            double p = 0.0;
+            for (int i = 0; i < m; ++i) p += scaled_sq(yh[i] - yl[i], a[i], yh[i], ctl.atol, ctl.rtol);
+            total = p;
+            count = m;
+            if (Coupled) {
+                double pd = 0.0;
+                for (int i = 0; i < m; ++i)
+                    for (int j = 0; j < 6; ++j)
+                        pd += scaled_sq(dh[i][j] - dl[i][j], da[i][j], dh[i][j], ctl.atol, ctl.rtol);
+                total = p + pd;
+                count += 6 * m;
+            }
+        } else {
+            double e0[6], e1[6], s0[6], sh[6], sl[6];
+            const double r0 = strain_at(eps_n, eps_np1, t, dt, e0);
+            const double r1 = strain_at(eps_n, eps_np1, t + hi, dt, e1);
+            if constexpr (Coupled) {
+                double C0[6][6], Ch[6][6], Cl[6][6];
+                stress_dual_pt(L, e0, r0, a, da, s0, C0);
+                stress_dual_pt(L, e1, r1, yh, dh, sh, Ch);
+                stress_dual_pt(L, e1, r1, yl, dl, sl, Cl);
+                double pc = 0.0;
+                for (int i = 0; i < 6; ++i)
+                    for (int j = 0; j < 6; ++j)
+                        pc += scaled_sq(Ch[i][j] - Cl[i][j], C0[i][j], Ch[i][j], ctl.atol, ctl.rtol);
+                double p = 0.0;
+                for (int i = 0; i < 6; ++i) p += scaled_sq(sh[i] - sl[i], s0[i], sh[i], ctl.atol, ctl.rtol);
+                total = p + pc;
+                count = 42;
+            } else {
+                (void)r0;
+                (void)r1;
+                stress_plain(L, e0, a, s0);
+                stress_plain(L, e1, yh, sh);
+                stress_plain(L, e1, yl, sl);
+                double p = 0.0;
+                for (int i = 0; i < 6; ++i) p += scaled_sq(sh[i] - sl[i], s0[i], sh[i], ctl.atol, ctl.rtol);
+                total = p;
+                count = 6;
+            }
+        }
+        double err = sqrt(total / count);
+        if (!(err - err == 0.0) || !ok) err = INFINITY;  // non-finite -> inf (odeint.py:617, 697)
+        const bool accept = err <= 1.0;
+        if (accept) {
+            t = clipped ? dt : t + hi;
+            for (int i = 0; i < m; ++i) {
+                a[i] = yh[i];
+                if (Coupled)
+                    for (int j = 0; j < 6; ++j) da[i][j] = dh[i][j];
+            }
+            ++substeps;
+            accepted_any = true;
+        } else {
+            ++rejected;
+        }
+        if (T::fsal) {  // odeint.py:712-723
+            const int src = accept ? s - 1 : 0;
+            for (int i = 0; i < m; ++i) {
+                g1[i] = G[src][i];
+                if (Coupled)
+                    for (int j = 0; j < 6; ++j) gd1[i][j] = Gd[src][i][j];
+            }
+            g1_valid = true;
+        }
+        // controller (odeint.py:729-738)
+        double factor = ctl.safety * pow(err, -1.0 / (T::order_low + 1.0));
+        if (err == 0.0) factor = ctl.max_factor;
+        if (factor != factor) factor = ctl.min_factor;
+        factor = fmin(fmax(factor, ctl.min_factor), ctl.max_factor);
+        double hn = hi * factor;
+        if (!accepted_any && !accept) hn = 0.5 * hi;
+        h = hn;
+        const bool done = accept && t >= dt * (1.0 - 1e-12);
+        if (substeps + rejected > ctl.max_substeps) return ST_INTEGRATION;
+        if (done) return 0;
+        if (h < 1e-14 * dt) return ST_INTEGRATION;  // step size underflow
+    }
+}
+
+}  // namespace am

@@ -28,10 +28,14 @@ struct KArgs {
     double* sigma;
     double* a_out;
     double* C;
-    int32_t* iters;
+    int32_t* iters;     // Newton count (implicit Euler) / accepted substeps (adaptive)
+    int32_t* rejected;  // rejected attempts (adaptive), optional
     uint8_t* status;
     uint32_t* flags;
     NewtonCfg ncfg;
+    int integrator;     // AM_INTEGRATOR_*
+    StepCtl sctl;
+    unsigned long long* sub_sum;  // optional: += accepted substeps of the adaptive kernels
 };
 
 // validation and dispatch (material.cu)
@@ -39,6 +43,9 @@ int check_law(const am_law* law);
 int check_cfg(const am_cfg* cfg);
 int law_m(const am_law* law);
 NewtonCfg newton_cfg(const am_cfg* cfg);
+StepCtl step_ctl(const am_cfg* cfg);
+// fills ncfg, integrator and sctl of k from cfg
+void set_controls(KArgs& k, const am_cfg* cfg);
 // enqueue K1 on stream s: Newton (+ clamp + stress), or with k.C the Newton
 // then tangent kernels; per-point status bits OR-ed into *k.flags
 int launch_material(const am_law* law, const KArgs& k, cudaStream_t s);

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "adaptive.cuh"
 #include "k1.cuh"
 #include "material.cuh"
 
@@ -177,18 +178,40 @@ int check_law(const am_law* law) {
 
 int check_cfg(const am_cfg* cfg) {
     if (!cfg) return fail(AM_ERR_ARG, "cfg is NULL");
-    if (cfg->strategy != AM_STRATEGY_AUTOMATIC || cfg->integrator != AM_INTEGRATOR_IMPLICIT_EULER)
+    const bool integ = cfg->integrator == AM_INTEGRATOR_IMPLICIT_EULER || cfg->integrator == AM_INTEGRATOR_ODE12 ||
+                       cfg->integrator == AM_INTEGRATOR_ODE23;
+    if (cfg->strategy != AM_STRATEGY_AUTOMATIC || !integ)
         return fail(AM_ERR_CONFIG,
-                    "only strategy='automatic' with integrator='implicit-euler' is implemented on the device "
+                    "the device implements strategy='automatic' with integrator implicit-euler, ode12 or ode23 "
                     "(got strategy %d, integrator %d)",
                     cfg->strategy, cfg->integrator);
     if (cfg->newton_mode != AM_NEWTON_INTERNAL && cfg->newton_mode != AM_NEWTON_STRESS)
         return fail(AM_ERR_CONFIG, "unknown newton mode %d", cfg->newton_mode);
+    if (cfg->error_measure != 0 && cfg->error_measure != 1)
+        return fail(AM_ERR_CONFIG, "unknown error measure %d", cfg->error_measure);
     if (cfg->max_newton <= 0) return fail(AM_ERR_ARG, "max_newton must be positive");
+    if (cfg->integrator != AM_INTEGRATOR_IMPLICIT_EULER && (cfg->max_substeps <= 0 || !(cfg->atol >= 0.0) ||
+                                                            !(cfg->rtol >= 0.0)))
+        return fail(AM_ERR_ARG, "bad step controller settings");
     return AM_OK;
 }
 
 NewtonCfg newton_cfg(const am_cfg* cfg) { return NewtonCfg{cfg->newton_mode, cfg->max_newton, cfg->newton_tol}; }
+
+StepCtl step_ctl(const am_cfg* cfg) {
+    StepCtl c;
+    c.atol = cfg->atol;
+    c.rtol = cfg->rtol;
+    c.max_substeps = cfg->max_substeps;
+    c.measure = cfg->error_measure;
+    return c;
+}
+
+void set_controls(KArgs& k, const am_cfg* cfg) {
+    k.ncfg = newton_cfg(cfg);
+    k.integrator = cfg->integrator;
+    k.sctl = step_ctl(cfg);
+}
 
 // Stream-ordered scratch comes from the device's default memory pool; keep
 // freed blocks in the pool (release threshold = max) so per-call
@@ -208,6 +231,61 @@ static void keep_pool_memory() {
     done.push_back(dev);
 }
 
+// adaptive explicit integrators (odeint.py:636-756): one thread per point;
+// substeps -> iters, rejected attempts -> rejected.  Coupled = tangent.
+template <class Law, int Scheme, bool Coupled>
+__global__ void __launch_bounds__(128) k_adaptive(Law L, KArgs k) {
+    constexpr int m = Law::m;
+    constexpr int ms = m > 0 ? m : 1;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
+        const PointIO io(k, b);
+        double en[6], ep[6], an[ms], a[ms], ac[ms], sig[6], da[ms][6];
+        io.eps(en, ep);
+        io.load_a<m>(k.a_n, an);
+        const double dt = io.dt();
+        int sub = 1, rej = 0, st = 0;
+        GlobalSink sink{k.C, k.lc.cs, b * k.lc.es};
+        if (dt == 0.0) {  // frozen (evaluator.py:142-150): a_n, elastic tangent, no clamp
+            for (int i = 0; i < m; ++i) ac[i] = an[i];
+            stress_plain(L, ep, an, sig);
+            if (Coupled) {
+                double C[6][6], s2[6];
+                stress_tangent(L, ep, an, nullptr, s2, C);
+                put_all(sink, C);
+            }
+        } else {
+            st = adaptive_point<Law, Scheme, Coupled>(L, k.sctl, en, an, ep, dt, a, da, sub, rej);
+            clamp_state<Law>(a, ac);  // evaluator.py:198
+            if (Coupled) {
+                double C[6][6];
+                stress_tangent(L, ep, ac, da, sig, C);  // evaluator.py:200
+                put_all(sink, C);
+            } else {
+                stress_plain(L, ep, ac, sig);
+            }
+        }
+        if (Coupled && !sink.finite) st |= ST_NONFINITE;
+        io.store_sigma(sig);
+        io.store_a<m>(ac);
+        if (k.iters) k.iters[b] = sub;
+        if (k.rejected) k.rejected[b] = rej;
+        if (k.sub_sum) {  // warp sum, one atomic per warp (integer: order independent)
+            const unsigned mask = __activemask();
+            const unsigned v = __reduce_add_sync(mask, (unsigned)sub);
+            if ((threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1)) atomicAdd(k.sub_sum, (unsigned long long)v);
+        }
+        io.status(st);
+    }
+}
+
+template <class Law, int Scheme>
+static int launch_adaptive(const Law& L, const KArgs& k, unsigned g, cudaStream_t s) {
+    if (k.C) k_adaptive<Law, Scheme, true><<<g, 128, 0, s>>>(L, k);
+    else k_adaptive<Law, Scheme, false><<<g, 128, 0, s>>>(L, k);
+    AM_CUDA(cudaGetLastError());
+    return AM_OK;
+}
+
 template <class Law>
 static int launch_law(const Law& L, KArgs k, cudaStream_t s) {
     const int threads = 128;
@@ -215,6 +293,10 @@ static int launch_law(const Law& L, KArgs k, cudaStream_t s) {
     if (blocks > (int64_t)kSMs * 1024) blocks = (int64_t)kSMs * 1024;
     const unsigned g = (unsigned)blocks;
     const bool stress = k.ncfg.mode == AM_NEWTON_STRESS;
+    if constexpr (Law::m > 0) {
+        if (k.integrator == AM_INTEGRATOR_ODE23) return launch_adaptive<Law, 23>(L, k, g, s);
+        if (k.integrator == AM_INTEGRATOR_ODE12) return launch_adaptive<Law, 12>(L, k, g, s);
+    }
     if (!k.C) {
         if (stress) k_material<Law, 1, false><<<g, threads, 0, s>>>(L, k);
         else k_material<Law, 0, false><<<g, threads, 0, s>>>(L, k);
@@ -260,7 +342,7 @@ using namespace am;
 extern "C" int am_eval_batch(const am_law* law, const am_cfg* cfg, int64_t B, const double* eps_n,
                              const double* a_n, const double* eps_np1, const double* dt, double dt_scalar,
                              int want_tangent, double* sigma, double* a_out, double* C, int32_t* newton_iters,
-                             uint8_t* status, uint32_t* flags, void* stream) {
+                             int32_t* rejected, uint8_t* status, uint32_t* flags, void* stream) {
     AM_TRY(check_law(law));
     AM_TRY(check_cfg(cfg));
     if (B < 0) return fail(AM_ERR_ARG, "negative batch size");
@@ -272,8 +354,8 @@ extern "C" int am_eval_batch(const am_law* law, const am_cfg* cfg, int64_t B, co
     k.eps_n = eps_n; k.a_n = a_n; k.eps_np1 = eps_np1; k.dt = dt; k.dt_scalar = dt_scalar;
     k.le = {B, 1}; k.la = {B, 1}; k.lc = {B, 1};
     k.sigma = sigma; k.a_out = a_out; k.C = want_tangent ? C : nullptr;
-    k.iters = newton_iters; k.status = status; k.flags = flags;
-    k.ncfg = newton_cfg(cfg);
+    k.iters = newton_iters; k.rejected = rejected; k.status = status; k.flags = flags;
+    set_controls(k, cfg);
     return launch_material(law, k, (cudaStream_t)stream);
 }
 
@@ -304,7 +386,7 @@ struct HostPipe {
             AM_CUDA(cudaStreamCreateWithFlags(&stream[s], cudaStreamNonBlocking));
             AM_CUDA(cudaMalloc(&in[s], sizeof(double) * chunk * 20));
             AM_CUDA(cudaMalloc(&out[s], sizeof(double) * chunk * 49));
-            AM_CUDA(cudaMalloc(&iters[s], sizeof(int32_t) * chunk));
+            AM_CUDA(cudaMalloc(&iters[s], sizeof(int32_t) * 2 * chunk));  // iters | rejected
             AM_CUDA(cudaMalloc(&status[s], chunk));
         }
         AM_CUDA(cudaMalloc(&flags, sizeof(uint32_t) * kSlots));
@@ -334,7 +416,8 @@ HostPipe& host_pipe() {
 
 extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t B, const double* eps_n,
                                   const double* a_n, const double* eps_np1, const double* dt, int want_tangent,
-                                  double* sigma, double* a_out, double* C, int32_t* newton_iters, uint8_t* status) {
+                                  double* sigma, double* a_out, double* C, int32_t* newton_iters,
+                                  int32_t* rejected, uint8_t* status) {
     AM_TRY(check_law(law));
     AM_TRY(check_cfg(cfg));
     if (B < 0) return fail(AM_ERR_ARG, "negative batch size");
@@ -369,8 +452,8 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
         k.eps_n = d_en; k.a_n = d_an; k.eps_np1 = d_e1; k.dt = d_dt; k.dt_scalar = 0.0;
         k.le = {1, 6}; k.la = {1, m}; k.lc = {1, 36};
         k.sigma = d_sig; k.a_out = d_ao; k.C = want_tangent ? d_C : nullptr;
-        k.iters = P.iters[s]; k.status = P.status[s]; k.flags = P.flags + s;
-        k.ncfg = newton_cfg(cfg);
+        k.iters = P.iters[s]; k.rejected = P.iters[s] + n; k.status = P.status[s]; k.flags = P.flags + s;
+        set_controls(k, cfg);
         AM_TRY(launch_material(law, k, st));
         AM_CUDA(cudaMemcpyAsync(sigma + 6 * lo, d_sig, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, st));
         if (m) AM_CUDA(cudaMemcpyAsync(a_out + m * lo, d_ao, sizeof(double) * m * n, cudaMemcpyDeviceToHost, st));
@@ -378,6 +461,8 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
             AM_CUDA(cudaMemcpyAsync(C + 36 * lo, d_C, sizeof(double) * 36 * n, cudaMemcpyDeviceToHost, st));
         if (newton_iters)
             AM_CUDA(cudaMemcpyAsync(newton_iters + lo, P.iters[s], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+        if (rejected)
+            AM_CUDA(cudaMemcpyAsync(rejected + lo, P.iters[s] + n, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
         if (status) AM_CUDA(cudaMemcpyAsync(status + lo, P.status[s], n, cudaMemcpyDeviceToHost, st));
     }
     uint32_t flags[HostPipe::kSlots];
@@ -387,6 +472,8 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
     for (int s = 0; s < HostPipe::kSlots; ++s) any |= flags[s];
     if (any & AM_VOXEL_NEWTON_FAILED)
         return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
+    if (any & AM_VOXEL_INTEGRATION)
+        return fail(AM_ERR_INTEGRATION, "adaptive integration: substep cap or step size underflow");
     if (any & AM_VOXEL_SINGULAR) return fail(AM_ERR_SINGULAR, "pivot below 1e-14 * max|A|");
     return AM_OK;
 }

@@ -162,13 +162,17 @@ __global__ void __launch_bounds__(kRedThreads) k_fourier(Spec sp, RefMat ref, do
 }
 
 // red[P*ny + 0..5] = Re S(origin) on the origin's owner (else 0),
-// red[P*ny + 6] = 1 if any material point failed
+// red[P*ny + 6] = 1 if a material point's Newton failed, [7] = 1 if an
+// adaptive integration hit a cap, [8] = accepted substeps of the adaptive
+// kernels in the sweep, [9] = 0 (summed over slabs: all exact)
 __global__ void k_finish(const double2* __restrict__ S, int64_t cs, int owner, const uint32_t* __restrict__ flags,
-                         double* __restrict__ red, int64_t off) {
+                         const unsigned long long* __restrict__ subs, double* __restrict__ red, int64_t off) {
     const int c = threadIdx.x;
     if (c < 6) red[off + c] = owner ? S[c * cs].x : 0.0;
     if (c == 6) red[off + 6] = (flags && (*flags & AM_VOXEL_NEWTON_FAILED)) ? 1.0 : 0.0;
-    if (c == 7) red[off + 7] = 0.0;
+    if (c == 7) red[off + 7] = (flags && (*flags & AM_VOXEL_INTEGRATION)) ? 1.0 : 0.0;
+    if (c == 8) red[off + 8] = subs ? (double)*subs : 0.0;
+    if (c == 9) red[off + 9] = 0.0;
 }
 
 // origin bin of the update: ehat(0) = N ebar, inverse-FFT input ebar
@@ -399,6 +403,7 @@ struct Slab {
     double2 *S = nullptr, *ehat = nullptr;   // spectra
     double2 *P = nullptr, *X = nullptr;      // 2-D spectra / exchange buffer (multi-slab)
     uint32_t* flags = nullptr;
+    unsigned long long* subs = nullptr;  // accepted substeps of the last sweep (adaptive integrators)
     std::vector<Phase> phases;
 };
 
@@ -407,6 +412,7 @@ struct Slab {
 struct am_solver {
     int nx = 0, ny = 0, nz = 0, nzh = 0;
     int64_t N = 0;
+    int64_t nstate = 0;  // voxels of phases with internal state (whole grid)
     int device = 0;
     cudaStream_t stream = nullptr;
     am_cfg cfg{};
@@ -448,7 +454,7 @@ static void solver_free(am_solver* h) {
             cudaFree(p.a_pend);
         }
         cudaFree(s.eps); cudaFree(s.eps_n); cudaFree(s.sigma);
-        cudaFree(s.S); cudaFree(s.ehat); cudaFree(s.P); cudaFree(s.X); cudaFree(s.flags);
+        cudaFree(s.S); cudaFree(s.ehat); cudaFree(s.P); cudaFree(s.X); cudaFree(s.flags); cudaFree(s.subs);
     }
     cudaFree(h->red); cudaFreeHost(h->hred);
     cudaFree(h->Cbuf); cudaFree(h->status); cudaFree(h->stats); cudaFreeHost(h->hstats); cudaFree(h->dsmall);
@@ -533,16 +539,18 @@ static int inverse(am_solver* h, double2* Slab::*src, double* Slab::*field) {
 static int material_sweep(am_solver* h, double dt) {
     for (auto& s : h->slabs) {
         AM_CUDA(cudaMemsetAsync(s.flags, 0, sizeof(uint32_t), h->stream));
+        AM_CUDA(cudaMemsetAsync(s.subs, 0, sizeof(unsigned long long), h->stream));
         for (auto& p : s.phases) {
             if (!p.count) continue;
             KArgs k{};
+            k.sub_sum = (p.m && h->cfg.integrator != AM_INTEGRATOR_IMPLICIT_EULER) ? s.subs : nullptr;
             k.B = p.count;
             k.gidx = p.gidx;
             k.eps_n = s.eps_n; k.eps_np1 = s.eps; k.a_n = p.a_n; k.dt = nullptr; k.dt_scalar = dt;
             k.le = {s.Nl, 1}; k.la = {p.count, 1}; k.lc = {0, 0};
             k.sigma = s.sigma; k.a_out = p.a_pend; k.C = nullptr;
             k.iters = nullptr; k.status = nullptr; k.flags = s.flags;
-            k.ncfg = newton_cfg(&h->cfg);
+            set_controls(k, &h->cfg);
             AM_TRY(launch_material(&p.law, k, h->stream));
         }
     }
@@ -560,7 +568,8 @@ static int fourier_pass(am_solver* h, bool update, std::vector<double>& out) {
         double* red = h->red + (int64_t)i * L;
         k_fourier<<<s.sp.nyl * kParts, kRedThreads, 0, h->stream>>>(s.sp, ref, s.S, s.ehat, red, update ? 1 : 0);
         AM_CUDA(cudaGetLastError());
-        k_finish<<<1, 32, 0, h->stream>>>(s.S, s.sp.cs, s.y0 == 0 ? 1 : 0, s.flags, red, (int64_t)h->ny * kParts);
+        k_finish<<<1, 32, 0, h->stream>>>(s.S, s.sp.cs, s.y0 == 0 ? 1 : 0, s.flags, s.subs, red,
+                                          (int64_t)h->ny * kParts);
         AM_CUDA(cudaGetLastError());
     }
     out.resize(L);
@@ -625,6 +634,8 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
         }
         AMC(cudaMalloc(&sl.flags, sizeof(uint32_t)));
         AMC(cudaMemset(sl.flags, 0, sizeof(uint32_t)));
+        AMC(cudaMalloc(&sl.subs, sizeof(unsigned long long)));
+        AMC(cudaMemset(sl.subs, 0, sizeof(unsigned long long)));
         // phases: slab-local sorted indices (the global order restricted to the slab)
         std::vector<std::vector<int64_t>> idx(nmat);
         const uint8_t* sid = ids + (int64_t)sl.x0 * ny * nz;
@@ -647,7 +658,9 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
             }
         }
     }
-    h->redlen = (int64_t)ny * kParts + 8;
+    h->redlen = (int64_t)ny * kParts + 10;
+    for (int64_t i = 0; i < N; ++i)
+        if (law_m(&laws[ids[i]])) ++h->nstate;
     AMC(cudaMalloc(&h->red, sizeof(double) * h->redlen * h->slabs.size()));
     AMC(cudaMallocHost(&h->hred, sizeof(double) * h->redlen * h->slabs.size()));
     h->chunk = std::min<int64_t>(Nl, int64_t(1) << 22);
@@ -806,10 +819,16 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
             AM_TRY(acc(2, 3, 2));
             h->t_ms[4] += 1.0;
         }
-        if (o[P + 6] != 0.0) {
+        if (o[P + 6] != 0.0 || o[P + 7] != 0.0) {
             info->iterations = it;
-            return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel (iteration %d)", it);
+            if (o[P + 6] != 0.0)
+                return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel (iteration %d)", it);
+            return fail(AM_ERR_INTEGRATION, "adaptive integration hit a cap (iteration %d)", it);
         }
+        // Homogenizer's mean substeps (homogenize.py:420-421): implicit Euler,
+        // frozen points and laws without state take one substep per voxel
+        if (h->cfg.integrator != AM_INTEGRATOR_IMPLICIT_EULER)
+            info->mean_substeps = (o[P + 8] + (double)(h->N - h->nstate)) / (double)h->N;
         double fsum = 0.0;
         for (int64_t i = 0; i < P; ++i) fsum += o[i];  // fixed order: ky plane, then part
         double sbar[6];
@@ -890,6 +909,7 @@ extern "C" int am_solver_evaluate(am_solver* h, double dt) {
         AM_CUDA(cudaMemcpyAsync(&f, s.flags, sizeof(f), cudaMemcpyDeviceToHost, h->stream));
         AM_CUDA(cudaStreamSynchronize(h->stream));
         if (f & AM_VOXEL_NEWTON_FAILED) bad = 1.0;
+        else if ((f & AM_VOXEL_INTEGRATION) && bad == 0.0) bad = 0.5;
     }
     if (h->comm) {
         AM_CUDA(cudaMemcpyAsync(h->dsmall, &bad, sizeof(double), cudaMemcpyHostToDevice, h->stream));
@@ -898,7 +918,8 @@ extern "C" int am_solver_evaluate(am_solver* h, double dt) {
         AM_CUDA(cudaStreamSynchronize(h->stream));
     }
     h->pending = true;
-    if (bad != 0.0) return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
+    if (bad == 1.0) return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
+    if (bad != 0.0) return fail(AM_ERR_INTEGRATION, "adaptive integration hit a cap");
     return AM_OK;
 }
 
@@ -936,7 +957,7 @@ extern "C" int am_solver_tangent_sweep(am_solver* h, double dt, double* Cbar, do
                 k.le = {s.Nl, 1}; k.la = {p.count, 1}; k.lc = {n, 1};
                 k.sigma = s.sigma; k.a_out = p.m ? p.a_pend + lo : nullptr; k.C = h->Cbuf;
                 k.iters = nullptr; k.status = h->status; k.flags = s.flags;
-                k.ncfg = newton_cfg(&h->cfg);
+                set_controls(k, &h->cfg);
                 AM_TRY(launch_material(&p.law, k, h->stream));
                 k_refstats<<<kRedBlocks, kRedThreads, 0, h->stream>>>(h->Cbuf, n, n, h->db, h->stats);
                 AM_CUDA(cudaGetLastError());
@@ -967,20 +988,23 @@ extern "C" int am_solver_tangent_sweep(am_solver* h, double dt, double* Cbar, do
         v[37] = (any & AM_VOXEL_NEWTON_FAILED) ? 1.0 : 0.0;
         v[38] = (any & AM_VOXEL_SINGULAR) ? 1.0 : 0.0;
         v[39] = (any & AM_VOXEL_NONFINITE) ? 1.0 : 0.0;
+        v[44] = (any & AM_VOXEL_INTEGRATION) ? 1.0 : 0.0;
         v[40] = st.kmin; v[41] = -st.kmax; v[42] = st.mlo; v[43] = -st.mhi;
         AM_CUDA(cudaMemcpyAsync(h->dsmall, v, sizeof(v), cudaMemcpyHostToDevice, h->stream));
         AM_NCCL(ncclAllReduce(h->dsmall, h->dsmall, 40, ncclDouble, ncclSum, h->comm, h->stream));
         AM_NCCL(ncclAllReduce(h->dsmall + 40, h->dsmall + 40, 4, ncclDouble, ncclMin, h->comm, h->stream));
+        AM_NCCL(ncclAllReduce(h->dsmall + 44, h->dsmall + 44, 1, ncclDouble, ncclSum, h->comm, h->stream));
         AM_CUDA(cudaMemcpyAsync(v, h->dsmall, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
         AM_CUDA(cudaStreamSynchronize(h->stream));
         for (int i = 0; i < 36; ++i) st.Csum[i] = v[i];
         st.bad = v[36];
         any = (v[37] > 0.0 ? AM_VOXEL_NEWTON_FAILED : 0u) | (v[38] > 0.0 ? AM_VOXEL_SINGULAR : 0u) |
-              (v[39] > 0.0 ? AM_VOXEL_NONFINITE : 0u);
+              (v[39] > 0.0 ? AM_VOXEL_NONFINITE : 0u) | (v[44] > 0.0 ? AM_VOXEL_INTEGRATION : 0u);
         st.kmin = v[40]; st.kmax = -v[41]; st.mlo = v[42]; st.mhi = -v[43];
     }
     h->pending = true;
     if (any & AM_VOXEL_NEWTON_FAILED) return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
+    if (any & AM_VOXEL_INTEGRATION) return fail(AM_ERR_INTEGRATION, "adaptive integration hit a cap");
     if (Cbar)
         for (int i = 0; i < 36; ++i) Cbar[i] = st.Csum[i] / (double)h->N;
     if (st.bad > 0.0 || (any & AM_VOXEL_NONFINITE))
@@ -1138,7 +1162,7 @@ extern "C" int am_green_apply_host(int nx, int ny, int nz, double lam, double mu
 extern "C" int am_equilibrium_residual_host(int nx, int ny, int nz, const double* sig, double* res) {
     if (nx <= 0 || ny <= 0 || nz <= 0 || !sig || !res) return fail(AM_ERR_ARG, "bad arguments");
     const Spec sp = spec_single(nx, ny, nz);
-    const int64_t N = sp.N, Nh = sp.cs, L = (int64_t)ny * kParts + 8;
+    const int64_t N = sp.N, Nh = sp.cs, L = (int64_t)ny * kParts + 10;
     double *f = nullptr, *red = nullptr;
     double2* c = nullptr;
     cufftHandle p1 = 0;
@@ -1157,7 +1181,7 @@ extern "C" int am_equilibrium_residual_host(int nx, int ny, int nz, const double
     if (rc == AM_OK && cufftExecD2Z(p1, f, c) != CUFFT_SUCCESS) rc = fail(AM_ERR_CUDA, "D2Z failed");
     if (rc == AM_OK) {
         k_fourier<<<ny * kParts, kRedThreads>>>(sp, RefMat::make(1.0, 1.0), c, nullptr, red, 0);
-        k_finish<<<1, 32>>>(c, sp.cs, 1, nullptr, red, (int64_t)ny * kParts);
+        k_finish<<<1, 32>>>(c, sp.cs, 1, nullptr, nullptr, red, (int64_t)ny * kParts);
         if (cudaMemcpy(o.data(), red, sizeof(double) * L, cudaMemcpyDeviceToHost) != cudaSuccess)
             rc = fail(AM_ERR_CUDA, "residual kernel failed");
     }

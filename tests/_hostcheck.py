@@ -44,3 +44,22 @@ def evaluate(law, eps_n, a_n, eps_np1, dt, want_tangent, newton_mode=0, tol=1e-1
         _p(dt), int(bool(want_tangent)), _p(sig), _p(a), _p(C),
         it.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
     return dict(sigma=sig, a=a[:, :m], C=C if want_tangent else None, iters=it, status=st, code=code)
+
+
+def adaptive(law, scheme, coupled, measure, eps_n, a_n, eps_np1, dt, atol=1e-6, rtol=1e-3, max_substeps=10000):
+    """Host build of the adaptive kernel (ode12 / ode23, automatic strategy)."""
+    kind, prm = law
+    eps_n = np.ascontiguousarray(eps_n, dtype=float)
+    eps_np1 = np.ascontiguousarray(eps_np1, dtype=float)
+    B = eps_np1.shape[0]
+    an = np.ascontiguousarray(a_n, dtype=float)
+    dt = np.ascontiguousarray(np.broadcast_to(np.asarray(dt, dtype=float), (B,)))
+    sig = np.zeros((B, 6)); a = np.zeros((B, 7)); C = np.zeros((B, 6, 6))
+    sub = np.zeros(B, np.int32); rej = np.zeros(B, np.int32); st = np.zeros(B, np.uint8)
+    i32 = ctypes.POINTER(ctypes.c_int32)
+    code = lib().hostcheck_adaptive(
+        _p(prm), int(scheme), int(bool(coupled)), 1 if measure == "stress" else 0, ctypes.c_double(atol),
+        ctypes.c_double(rtol), int(max_substeps), ctypes.c_int64(B), _p(eps_n), _p(an), _p(eps_np1), _p(dt),
+        _p(sig), _p(a), _p(C), sub.ctypes.data_as(i32), rej.ctypes.data_as(i32),
+        st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+    return dict(sigma=sig, a=a, C=C if coupled else None, substeps=sub, rejected=rej, status=st, code=code)

@@ -174,6 +174,45 @@ def make_material():
     save("material_edge.npz", **out)
 
 
+# ---------------------------------------------------------------- adaptive integrators
+def make_adaptive():
+    """ode12 / ode23 (automatic strategy), internal and stress error measures,
+    with and without the coupled tangent: sigma, a, C, substeps, rejected."""
+    law = gsm.MichelSuquet()
+    out = {}
+    en, an, ep, dt = W.config2_batch(192, seed=21)
+    dt = dt.copy()
+    dt[64:128] = 10.0 ** np.random.default_rng(22).uniform(-3, 1, 64)  # varied step lengths
+    dt[128:136] = 0.0  # frozen points inside an adaptive batch
+    out.update(eps_n=en, a_n=an, eps_np1=ep, dt=dt)
+    for integ in ("ode12", "ode23"):
+        for meas in ("internal", "stress"):
+            cfg = StrategyConfig(strategy="automatic", integrator=integ, error_measure=meas)
+            for tang in (False, True):
+                t0 = time.time()
+                r = evaluate_arrays(law, cfg, en, an, ep, dt, want_tangent=tang)
+                tag = f"{integ}_{meas}_{'t' if tang else 'n'}"
+                out[tag + "_sigma"] = r.sigma
+                out[tag + "_a"] = r.a
+                out[tag + "_substeps"] = r.substeps
+                out[tag + "_rejected"] = r.rejected
+                if tang:
+                    out[tag + "_C"] = r.C
+                print(f"adaptive {tag}: {time.time() - t0:.1f}s, substeps {r.substeps.sum()}, rejected {r.rejected.sum()}")
+    # IntegrationError: substep cap on large increments
+    cfg = StrategyConfig(strategy="automatic", integrator="ode23", max_substeps=3)
+    e2 = np.zeros((4, 6))
+    p2 = np.random.default_rng(23).normal(0, 1e-2, (4, 6))
+    try:
+        evaluate_arrays(law, cfg, e2, np.zeros((4, 7)), p2, np.full(4, 1.0), want_tangent=True)
+        err = ""
+    except Exception as exc:  # noqa: BLE001
+        err = type(exc).__name__
+    out.update(cap_eps_np1=p2, cap_err=np.array(err))
+    print("cap case:", err)
+    save("adaptive.npz", **out)
+
+
 # ---------------------------------------------------------------- constitutive
 def make_constitutive():
     law = gsm.MichelSuquet()
@@ -347,6 +386,7 @@ if __name__ == "__main__":
     args = ap.parse_args()
     jobs = {
         "material": make_material,
+        "adaptive": make_adaptive,
         "constitutive": make_constitutive,
         "fourier": make_fourier,
         "config1": make_config1,

@@ -73,3 +73,56 @@ extern "C" int hostcheck_eval(int kind, const double* prm, int mode, double tol,
     auto L = LinearElasticLaw::make(prm[0], prm[1]);
     return run(L, cfg, B, eps_n, a_n, eps_np1, dt, want_tangent, sig, a_out, C, iters, status);
 }
+
+// adaptive ode12 / ode23 (material.cu k_adaptive on the host)
+#include "../../paper_2006_04391_b200/csrc/adaptive.cuh"
+
+template <int Scheme, bool Coupled>
+static int run_adaptive(const MichelSuquetLaw& L, const StepCtl& ctl, int64_t B, const double* eps_n,
+                        const double* a_n, const double* eps_np1, const double* dt, double* sig, double* a_out,
+                        double* C, int32_t* sub, int32_t* rej, uint8_t* status) {
+    int any = 0;
+    for (int64_t b = 0; b < B; ++b) {
+        const double *en = eps_n + 6 * b, *ep = eps_np1 + 6 * b, *an = a_n + 7 * b;
+        double a[7], ac[7], da[7][6], Cv[6][6];
+        int s = 1, r = 0, st = 0;
+        HostSink sink{Cv};
+        if (dt[b] == 0.0) {
+            for (int i = 0; i < 7; ++i) ac[i] = an[i];
+            stress_plain(L, ep, an, sig + 6 * b);
+            if (Coupled) {
+                double s2[6];
+                stress_tangent(L, ep, an, nullptr, s2, Cv);
+            }
+        } else {
+            st = adaptive_point<MichelSuquetLaw, Scheme, Coupled>(L, ctl, en, an, ep, dt[b], a, da, s, r);
+            clamp_state<MichelSuquetLaw>(a, ac);
+            if (Coupled) stress_tangent(L, ep, ac, da, sig + 6 * b, Cv);
+            else stress_plain(L, ep, ac, sig + 6 * b);
+        }
+        std::memcpy(a_out + 7 * b, ac, sizeof(ac));
+        if (Coupled) std::memcpy(C + 36 * b, Cv, sizeof(Cv));
+        sub[b] = s;
+        rej[b] = r;
+        status[b] = (uint8_t)st;
+        any |= st;
+    }
+    return any;
+}
+
+extern "C" int hostcheck_adaptive(const double* prm, int scheme, int coupled, int measure, double atol, double rtol,
+                                  int max_sub, int64_t B, const double* eps_n, const double* a_n, const double* eps_np1,
+                                  const double* dt, double* sig, double* a_out, double* C, int32_t* sub, int32_t* rej,
+                                  uint8_t* status) {
+    auto L = MichelSuquetLaw::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]);
+    StepCtl ctl;
+    ctl.atol = atol;
+    ctl.rtol = rtol;
+    ctl.max_substeps = max_sub;
+    ctl.measure = measure;
+    if (scheme == 23)
+        return coupled ? run_adaptive<23, true>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status)
+                       : run_adaptive<23, false>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status);
+    return coupled ? run_adaptive<12, true>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status)
+                   : run_adaptive<12, false>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status);
+}

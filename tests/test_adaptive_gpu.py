@@ -1,0 +1,78 @@
+"""Adaptive ode12 / ode23 on the GPU (k_adaptive through evaluate_arrays) vs
+the reference's results (tests/golden/adaptive.npz): identical accepted and
+rejected substep counts, sigma / a within 1e-10, C within 1e-8."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from _util import TOL_STATE, TOL_TANGENT, assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2006_04391_b200 import gsm
+    from paper_2006_04391_b200.evaluator import StrategyConfig, evaluate_arrays
+
+    return gsm, StrategyConfig, evaluate_arrays
+
+
+@pytest.mark.parametrize("integ", ["ode12", "ode23"])
+@pytest.mark.parametrize("meas", ["internal", "stress"])
+@pytest.mark.parametrize("tang", [False, True])
+def test_adaptive_vs_reference(api, integ, meas, tang):
+    gsm, SC, ev = api
+    g = golden("adaptive.npz")
+    tag = f"{integ}_{meas}_{'t' if tang else 'n'}"
+    cfg = SC(strategy="automatic", integrator=integ, error_measure=meas)
+    r = ev(gsm.MichelSuquet(), cfg, g["eps_n"], g["a_n"], g["eps_np1"], g["dt"], want_tangent=tang)
+    assert np.array_equal(r.substeps, g[tag + "_substeps"])
+    assert np.array_equal(r.rejected, g[tag + "_rejected"])
+    assert_close(r.sigma, g[tag + "_sigma"], TOL_STATE, "sigma")
+    assert_close(r.a, g[tag + "_a"], TOL_STATE, "a")
+    if tang:
+        assert_close(r.C, g[tag + "_C"], TOL_TANGENT, "C")
+
+
+def test_default_config_is_ode23(api):
+    gsm, SC, ev = api
+    g = golden("adaptive.npz")
+    r = ev(gsm.MichelSuquet(), SC(), g["eps_n"], g["a_n"], g["eps_np1"], g["dt"], want_tangent=True)
+    assert np.array_equal(r.substeps, g["ode23_internal_t_substeps"])
+
+
+def test_integration_error(api):
+    gsm, SC, ev = api
+    from paper_2006_04391_b200.odeint import IntegrationError
+
+    g = golden("adaptive.npz")
+    cfg = SC(strategy="automatic", integrator="ode23", max_substeps=3)
+    with pytest.raises(IntegrationError):
+        ev(gsm.MichelSuquet(), cfg, np.zeros((4, 6)), np.zeros((4, 7)), g["cap_eps_np1"], 1.0, want_tangent=True)
+
+
+def test_record_steps_rejected(api):
+    gsm, SC, ev = api
+    from paper_2006_04391_b200.evaluator import ConfigError
+
+    with pytest.raises(ConfigError):
+        ev(gsm.MichelSuquet(), SC(record_steps=True), np.zeros((2, 6)), np.zeros((2, 7)), np.zeros((2, 6)), 0.1)
+
+
+def test_basic_scheme_with_ode23(api):
+    """The basic scheme accepts the adaptive integrator: config 1 (elastic, so
+    identical to implicit Euler) and one EVP step on 8^3 against implicit
+    Euler to the integrators' agreement level."""
+    gsm, SC, _ = api
+    from paper_2006_04391_b200 import homogenize as H
+
+    g = golden("config1.npz")
+    grid = H.VoxelGrid(g["ids"], [gsm.LinearElastic(55e9, 0.33), gsm.LinearElastic(300e9, 0.25)])
+    eb = np.zeros(6)
+    eb[0] = 1e-3
+    eps, sig, info = H.Homogenizer(grid, SC()).solve_step(eb, 1.0)
+    assert info.iterations == int(g["strain_iters"])
+    recs = H.run_loading_path(H.toy_mmc_grid(8), H.LoadingPath(steps=20), SC())[:2]
+    assert all(r["mean_substeps"] >= 1.0 for r in recs)

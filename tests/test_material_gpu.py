@@ -124,7 +124,7 @@ def test_device_soa_entry_matches_host_entry(api):
     lib = _lib.load()
     rc = lib.am_eval_batch(
         _lib.make_law(gsm.MichelSuquet()), _lib.make_cfg(cfg), B, d_en.data_ptr(), d_an.data_ptr(), d_ep.data_ptr(),
-        None, 0.05, 1, d_sig.data_ptr(), d_a.data_ptr(), d_C.data_ptr(), d_it.data_ptr(), d_st.data_ptr(),
+        None, 0.05, 1, d_sig.data_ptr(), d_a.data_ptr(), d_C.data_ptr(), d_it.data_ptr(), None, d_st.data_ptr(),
         d_fl.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     _lib.check(rc)
     torch.cuda.synchronize()

@@ -38,7 +38,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--one":
             def step():
                 _lib.check(lib.am_eval_batch(law, cfg, B, d_en.data_ptr(), d_an.data_ptr(), d_ep.data_ptr(), None,
                                              0.05, tang, d_sig.data_ptr(), d_a.data_ptr(),
-                                             d_C.data_ptr() if tang else None, d_it.data_ptr(), None, None, None))
+                                             d_C.data_ptr() if tang else None, d_it.data_ptr(), None, None, None, None))
             for _ in range(3):
                 step()
             torch.cuda.synchronize()
