@@ -210,6 +210,29 @@ def make_adaptive():
         err = type(exc).__name__
     out.update(cap_eps_np1=p2, cap_err=np.array(err))
     print("cap case:", err)
+    # basic scheme with the default StrategyConfig() (ode23): 8^3 toy grid,
+    # load step 1 converges; step 2 stagnates near 5e-4 (the adaptive step
+    # selection makes sigma(eps) non-smooth) and raises SolverError
+    grid = H.toy_mmc_grid(8)
+    hom = H.Homogenizer(grid, StrategyConfig(), max_iterations=400)
+    path = H.LoadingPath(steps=20)
+    tt = path.times()
+    ex = path.eps_xx(tt)
+    free = np.array([False] + [True] * 5)
+    eb = np.zeros(6)
+    eb[0] = ex[1]
+    eps, sig, info = hom.solve_step(eb, tt[1] - tt[0], free_mask=free)
+    out.update(path8_ode23_iters=np.array(info.iterations), path8_ode23_mean_substeps=np.array(info.mean_substeps),
+               path8_ode23_history=np.array(info.history), path8_ode23_sig_bar=sig.mean(axis=(1, 2, 3)))
+    hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+    eb[0] = ex[2]
+    try:
+        hom.solve_step(eb, tt[2] - tt[1], free_mask=free)
+        err = ""
+    except H.SolverError:
+        err = "SolverError"
+    out.update(path8_ode23_step2_err=np.array(err))
+    print("path8 ode23:", info.iterations, info.mean_substeps, err)
     save("adaptive.npz", **out)
 
 

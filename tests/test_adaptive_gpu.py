@@ -62,17 +62,27 @@ def test_record_steps_rejected(api):
 
 
 def test_basic_scheme_with_ode23(api):
-    """The basic scheme accepts the adaptive integrator: config 1 (elastic, so
-    identical to implicit Euler) and one EVP step on 8^3 against implicit
-    Euler to the integrators' agreement level."""
+    """The basic scheme with the default StrategyConfig() (ode23) on the 8^3
+    toy grid: load step 1 as the reference (iterations, mean substeps,
+    history, mean stress); load step 2 stagnates near 5e-4 and raises
+    SolverError, as in the reference."""
     gsm, SC, _ = api
     from paper_2006_04391_b200 import homogenize as H
 
-    g = golden("config1.npz")
-    grid = H.VoxelGrid(g["ids"], [gsm.LinearElastic(55e9, 0.33), gsm.LinearElastic(300e9, 0.25)])
+    g = golden("adaptive.npz")
+    hom = H.Homogenizer(H.toy_mmc_grid(8), SC(), max_iterations=400)
+    path = H.LoadingPath(steps=20)
+    t, ex = path.times(), path.eps_xx(path.times())
+    free = np.array([False] + [True] * 5)
     eb = np.zeros(6)
-    eb[0] = 1e-3
-    eps, sig, info = H.Homogenizer(grid, SC()).solve_step(eb, 1.0)
-    assert info.iterations == int(g["strain_iters"])
-    recs = H.run_loading_path(H.toy_mmc_grid(8), H.LoadingPath(steps=20), SC())[:2]
-    assert all(r["mean_substeps"] >= 1.0 for r in recs)
+    eb[0] = ex[1]
+    eps, sig, info = hom.solve_step(eb, t[1] - t[0], free_mask=free)
+    assert info.iterations == int(g["path8_ode23_iters"])
+    assert info.mean_substeps == float(g["path8_ode23_mean_substeps"])
+    assert np.max(np.abs(np.array(info.history) / g["path8_ode23_history"] - 1)) < 1e-6
+    assert_close(sig.mean(axis=(1, 2, 3)), g["path8_ode23_sig_bar"], 1e-8)
+    hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+    eb[0] = ex[2]
+    assert str(g["path8_ode23_step2_err"]) == "SolverError"
+    with pytest.raises(H.SolverError):
+        hom.solve_step(eb, t[2] - t[1], free_mask=free)
