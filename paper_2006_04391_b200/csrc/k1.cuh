@@ -34,6 +34,7 @@ struct KArgs {
     uint32_t* flags;
     NewtonCfg ncfg;
     int integrator;     // AM_INTEGRATOR_*
+    int strategy;       // AM_STRATEGY_*
     StepCtl sctl;
     unsigned long long* sub_sum;  // optional: += accepted substeps of the adaptive kernels
 };

@@ -180,10 +180,11 @@ int check_cfg(const am_cfg* cfg) {
     if (!cfg) return fail(AM_ERR_ARG, "cfg is NULL");
     const bool integ = cfg->integrator == AM_INTEGRATOR_IMPLICIT_EULER || cfg->integrator == AM_INTEGRATOR_ODE12 ||
                        cfg->integrator == AM_INTEGRATOR_ODE23;
-    if (cfg->strategy != AM_STRATEGY_AUTOMATIC || !integ)
+    const bool strat = cfg->strategy == AM_STRATEGY_AUTOMATIC || cfg->strategy == AM_STRATEGY_SEMI_AUTOMATIC;
+    if (!strat || !integ)
         return fail(AM_ERR_CONFIG,
-                    "the device implements strategy='automatic' with integrator implicit-euler, ode12 or ode23 "
-                    "(got strategy %d, integrator %d)",
+                    "the device implements the automatic and semi-automatic strategies with integrator "
+                    "implicit-euler, ode12 or ode23 (got strategy %d, integrator %d)",
                     cfg->strategy, cfg->integrator);
     if (cfg->newton_mode != AM_NEWTON_INTERNAL && cfg->newton_mode != AM_NEWTON_STRESS)
         return fail(AM_ERR_CONFIG, "unknown newton mode %d", cfg->newton_mode);
@@ -210,6 +211,7 @@ StepCtl step_ctl(const am_cfg* cfg) {
 void set_controls(KArgs& k, const am_cfg* cfg) {
     k.ncfg = newton_cfg(cfg);
     k.integrator = cfg->integrator;
+    k.strategy = cfg->strategy;
     k.sctl = step_ctl(cfg);
 }
 
@@ -327,9 +329,16 @@ static int launch_law(const Law& L, KArgs k, cudaStream_t s) {
 
 int launch_material(const am_law* law, const KArgs& k, cudaStream_t s) {
     if (k.B == 0) return AM_OK;
-    if (law->kind == AM_LAW_MICHEL_SUQUET)
+    const bool semi = k.strategy == AM_STRATEGY_SEMI_AUTOMATIC;
+    if (law->kind == AM_LAW_MICHEL_SUQUET) {
+        if (semi)
+            return launch_law(SemiLaw<MichelSuquetLaw>::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot,
+                                                             law->sigma_d, law->n),
+                              k, s);
         return launch_law(
             MichelSuquetLaw::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot, law->sigma_d, law->n), k, s);
+    }
+    if (semi) return launch_law(SemiLaw<LinearElasticLaw>::make(law->E, law->nu), k, s);
     return launch_law(LinearElasticLaw::make(law->E, law->nu), k, s);
 }
 

@@ -17,6 +17,7 @@
 
 #include "ad.cuh"
 #include "laws.cuh"
+#include "semi.cuh"
 
 #include "newton_cfg.cuh"
 
@@ -56,21 +57,31 @@ AM_HD auto negs_of(const T& t, std::integer_sequence<int, I...>) {
 
 // ---------------------------------------------------------------- LawOps sweeps
 // stress_generic (gsm.py:431-439): eps leaves, a constants
+// (semi-automatic: the hand partials of semi.cuh, gsm.py:431-458)
 template <class Law, class PE, class PA>
 AM_HD auto stress_sweep(const Law& L, const PE& pe, const PA& pa) {
-    auto w = L.omega(leaves_of(pe, seq<6>{}), csts_of(pa, seq<Law::m>{}));
-    return grads_of(w, pe, seq<6>{});
+    if constexpr (is_semi_v<Law>) {
+        return L.hand_stress(pe, pa);
+    } else {
+        auto w = L.omega(leaves_of(pe, seq<6>{}), csts_of(pa, seq<Law::m>{}));
+        return grads_of(w, pe, seq<6>{});
+    }
 }
 // gen_stress_generic (gsm.py:441-449): eps constants, a leaves, A = -adj
 template <class Law, class PE, class PA>
 AM_HD auto gen_stress_sweep(const Law& L, const PE& pe, const PA& pa) {
-    auto w = L.omega(csts_of(pe, seq<6>{}), leaves_of(pa, seq<Law::m>{}));
-    return negs_of(grads_of(w, pa, seq<Law::m>{}), seq<Law::m>{});
+    if constexpr (is_semi_v<Law>) {
+        return L.hand_gen_stress(pe, pa);
+    } else {
+        auto w = L.omega(csts_of(pe, seq<6>{}), leaves_of(pa, seq<Law::m>{}));
+        return negs_of(grads_of(w, pa, seq<Law::m>{}), seq<Law::m>{});
+    }
 }
 // flow_generic (gsm.py:451-458)
 template <class Law, class PA>
 AM_HD auto flow_sweep(const Law& L, const PA& A) {
-    return grads_of(L.psi(leaves_of(A, seq<Law::m>{})), A, seq<Law::m>{});
+    if constexpr (is_semi_v<Law>) return L.hand_flow(A);
+    else return grads_of(L.psi(leaves_of(A, seq<Law::m>{})), A, seq<Law::m>{});
 }
 // rhs_generic (gsm.py:460-461)
 template <class Law, class PE, class PA>
@@ -82,6 +93,15 @@ AM_HD auto rhs_sweep(const Law& L, const PE& pe, const PA& pa) {
 // rhs_and_jacobians (gsm.py:494-518) the Newton iteration consumes.
 template <class Law>
 AM_HD void rhs_jac_a(const Law& L, const double* e, const double* a, double* f, double (*J)[Law::m]) {
+    if constexpr (is_semi_v<Law>) {  // rhs_jac_generic (gsm.py:463-481)
+        double J6[Law::m][6];
+        L.rhs_jac(e, a, f, J6, nullptr);
+        for (int i = 0; i < Law::m; ++i) {
+            for (int k = 0; k < 6; ++k) J[i][k] = J6[i][k];
+            J[i][6] = 0.0;
+        }
+        return;
+    }
     auto fv = rhs_sweep(L, plain_tup<6>(e, seq<6>{}), seed_tup<0>(a, 1.0, seq<Law::m>{}));
     sfor<Law::m>([&](auto I) {
         constexpr int i = decltype(I)::value;
@@ -118,9 +138,34 @@ AM_HD auto da_tup(const double* a, const double (*da)[6], std::integer_sequence<
 }
 
 // stress_and_tangent (gsm.py:520-551): sigma and C[i][j] = dsigma_i/deps_j
+// semi-automatic: sigma by hand, C = d2w_ee + d2w_ae^T da (gsm.py:531-536)
+template <class Law>
+AM_HD void semi_stress_tangent_cols(const Law& L, const double* e, const double* a, const double* dacol,
+                                    int dstride, int j, double* sig, double* c) {
+    stress_plain(L, e, a, sig);
+    double Ce[6][6];
+    L.Ce(Ce);
+    for (int i = 0; i < 6; ++i) {
+        double s = 0.0;
+        if (dacol) {  // einsum("ki,kj->ij", d2w_ae, da): d2w_ae = [-Ce; 0]
+            for (int k = 0; k < 6; ++k) s += (-Ce[k][i]) * dacol[k * dstride];
+            if (Law::m > 6) s += 0.0 * dacol[6 * dstride];
+        }
+        c[i] = dacol ? Ce[i][j] + s : Ce[i][j];
+    }
+}
+
 template <class Law>
 AM_HD void stress_tangent(const Law& L, const double* e, const double* a, const double (*da)[6], double* sig,
                           double (*C)[6]) {
+    if constexpr (is_semi_v<Law>) {
+        for (int j = 0; j < 6; ++j) {
+            double c[6];
+            semi_stress_tangent_cols(L, e, a, (Law::m && da) ? &da[0][j] : nullptr, 6, j, sig, c);
+            for (int i = 0; i < 6; ++i) C[i][j] = c[i];
+        }
+        return;
+    }
     auto pe = seed_tup<0>(e, 1.0, seq<6>{});
     auto run = [&](const auto& pa) {
         auto s = stress_sweep(L, pe, pa);
@@ -287,14 +332,21 @@ struct JacShape {
     using FT = decltype(rhs_sweep(std::declval<const Law&>(), plain_tup<6>((const double*)nullptr, seq<6>{}),
                                   seed_tup<0>((const double*)nullptr, 1.0, seq<m>{})));
     static constexpr uint32_t mask = tup_mask<FT>(seq<m>{});
-    // dense block = leading columns when the nonzero columns are a prefix
-    static constexpr int nd = (mask == ((1u << popc(mask)) - 1u)) ? popc(mask) : m;
+    // dense block = leading columns when the nonzero columns are a prefix;
+    // the semi-automatic Jacobian has an explicitly empty last column
+    // (d2w_aa's last row and column vanish, gsm.py:221-225)
+    static constexpr int nd = is_semi_v<Law> ? m - 1 : (mask == ((1u << popc(mask)) - 1u)) ? popc(mask) : m;
     static constexpr int nr = m - nd;
 };
 
 // f and the nd leading (structurally nonzero) columns of df/da
 template <class Law, int nd>
 AM_HD void rhs_jac_dense(const Law& L, const double* e, const double* a, double* f, double (*J)[nd]) {
+    if constexpr (is_semi_v<Law>) {
+        static_assert(nd == 6, "semi-automatic Jacobian has 6 dense columns");
+        L.rhs_jac(e, a, f, J, nullptr);
+        return;
+    }
     auto fv = rhs_sweep(L, plain_tup<6>(e, seq<6>{}), seed_tup<0>(a, 1.0, seq<Law::m>{}));
     sfor<Law::m>([&](auto I) {
         constexpr int i = decltype(I)::value;
@@ -472,6 +524,15 @@ AM_HD void tangent_block(const Law& L, const double* e1, double r, double h, con
 #pragma unroll
         for (int i = 0; i < m; ++i) da[i][jj] = x[i];
     });
+    if constexpr (is_semi_v<Law>) {
+        sfor<NJ>([&](auto Jc) {
+            constexpr int jj = decltype(Jc)::value;
+            double c[6];
+            semi_stress_tangent_cols(L, eps_np1, ac, &da[0][jj], NJ, J0 + jj, sig, c);
+            sink.col(J0 + jj, c);
+        });
+        return;
+    }
     auto s = stress_sweep(L, eps_seed_block<J0, NJ>(eps_np1, 1.0, seq<6>{}), da_block_tup<NJ>(ac, da, seq<m>{}));
     sfor<NJ>([&](auto Jc) {
         constexpr int jj = decltype(Jc)::value;

@@ -29,7 +29,7 @@ def _p(a):
     return a.ctypes.data_as(_dp)
 
 
-def evaluate(law, eps_n, a_n, eps_np1, dt, want_tangent, newton_mode=0, tol=1e-10):
+def evaluate(law, eps_n, a_n, eps_np1, dt, want_tangent, newton_mode=0, tol=1e-10, semi=False):
     kind, prm = law
     m = 7 if kind == 1 else 0
     eps_n = np.ascontiguousarray(eps_n, dtype=float)
@@ -42,11 +42,13 @@ def evaluate(law, eps_n, a_n, eps_np1, dt, want_tangent, newton_mode=0, tol=1e-1
     code = lib().hostcheck_eval(
         kind, _p(prm), int(newton_mode), ctypes.c_double(tol), ctypes.c_int64(B), _p(eps_n), _p(an), _p(eps_np1),
         _p(dt), int(bool(want_tangent)), _p(sig), _p(a), _p(C),
-        it.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+        it.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+        int(bool(semi)))
     return dict(sigma=sig, a=a[:, :m], C=C if want_tangent else None, iters=it, status=st, code=code)
 
 
-def adaptive(law, scheme, coupled, measure, eps_n, a_n, eps_np1, dt, atol=1e-6, rtol=1e-3, max_substeps=10000):
+def adaptive(law, scheme, coupled, measure, eps_n, a_n, eps_np1, dt, atol=1e-6, rtol=1e-3, max_substeps=10000,
+             semi=False):
     """Host build of the adaptive kernel (ode12 / ode23, automatic strategy)."""
     kind, prm = law
     eps_n = np.ascontiguousarray(eps_n, dtype=float)
@@ -61,5 +63,5 @@ def adaptive(law, scheme, coupled, measure, eps_n, a_n, eps_np1, dt, atol=1e-6, 
         _p(prm), int(scheme), int(bool(coupled)), 1 if measure == "stress" else 0, ctypes.c_double(atol),
         ctypes.c_double(rtol), int(max_substeps), ctypes.c_int64(B), _p(eps_n), _p(an), _p(eps_np1), _p(dt),
         _p(sig), _p(a), _p(C), sub.ctypes.data_as(i32), rej.ctypes.data_as(i32),
-        st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+        st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), int(bool(semi)))
     return dict(sigma=sig, a=a, C=C if coupled else None, substeps=sub, rejected=rej, status=st, code=code)

@@ -236,6 +236,40 @@ def make_adaptive():
     save("adaptive.npz", **out)
 
 
+# ---------------------------------------------------------------- semi-automatic strategy
+def make_semi():
+    """strategy='semi-automatic' (hand partials, gsm.py:258-328, 463-481):
+    implicit Euler with Newton counts, and ode23 / ode12, with and without tangent."""
+    law = gsm.MichelSuquet()
+    out = {}
+    en, an, ep, dt = W.config2_batch(256, seed=31)
+    dt = dt.copy()
+    dt[200:232] = 10.0 ** np.random.default_rng(32).uniform(-3, 1, 32)
+    dt[232:240] = 0.0
+    out.update(eps_n=en, a_n=an, eps_np1=ep, dt=dt)
+    SEMI = StrategyConfig(strategy="semi-automatic", integrator="implicit-euler")
+    for tang in (False, True):
+        r, cnt, err = eval_counted(law, SEMI, en, an, ep, dt, tang)
+        assert not err
+        tag = f"ie_{'t' if tang else 'n'}"
+        out[tag + "_sigma"], out[tag + "_a"], out[tag + "_iters"] = r.sigma, r.a, cnt
+        if tang:
+            out[tag + "_C"] = r.C
+    for integ in ("ode12", "ode23"):
+        cfg = StrategyConfig(strategy="semi-automatic", integrator=integ)
+        for tang in (False, True):
+            r = evaluate_arrays(law, cfg, en, an, ep, dt, want_tangent=tang)
+            tag = f"{integ}_{'t' if tang else 'n'}"
+            out[tag + "_sigma"], out[tag + "_a"] = r.sigma, r.a
+            out[tag + "_substeps"], out[tag + "_rejected"] = r.substeps, r.rejected
+            if tang:
+                out[tag + "_C"] = r.C
+    le = gsm.LinearElastic(300e9, 0.25)
+    r = evaluate_arrays(le, SEMI, en, np.zeros((256, 0)), ep, dt, want_tangent=True)
+    out.update(le_sigma=r.sigma, le_C=r.C)
+    save("material_semi.npz", **out)
+
+
 # ---------------------------------------------------------------- constitutive
 def make_constitutive():
     law = gsm.MichelSuquet()
@@ -410,6 +444,7 @@ if __name__ == "__main__":
     jobs = {
         "material": make_material,
         "adaptive": make_adaptive,
+        "semi": make_semi,
         "constitutive": make_constitutive,
         "fourier": make_fourier,
         "config1": make_config1,

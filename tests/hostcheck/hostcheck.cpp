@@ -64,10 +64,18 @@ static int run(const Law& L, const NewtonCfg& cfg, int64_t B, const double* eps_
 
 extern "C" int hostcheck_eval(int kind, const double* prm, int mode, double tol, int64_t B, const double* eps_n,
                               const double* a_n, const double* eps_np1, const double* dt, int want_tangent,
-                              double* sig, double* a_out, double* C, int32_t* iters, uint8_t* status) {
+                              double* sig, double* a_out, double* C, int32_t* iters, uint8_t* status, int semi) {
     NewtonCfg cfg{mode, 50, tol};
     if (kind == 1) {
+        if (semi) {
+            auto L = SemiLaw<MichelSuquetLaw>::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]);
+            return run(L, cfg, B, eps_n, a_n, eps_np1, dt, want_tangent, sig, a_out, C, iters, status);
+        }
         auto L = MichelSuquetLaw::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]);
+        return run(L, cfg, B, eps_n, a_n, eps_np1, dt, want_tangent, sig, a_out, C, iters, status);
+    }
+    if (semi) {
+        auto L = SemiLaw<LinearElasticLaw>::make(prm[0], prm[1]);
         return run(L, cfg, B, eps_n, a_n, eps_np1, dt, want_tangent, sig, a_out, C, iters, status);
     }
     auto L = LinearElasticLaw::make(prm[0], prm[1]);
@@ -77,8 +85,8 @@ extern "C" int hostcheck_eval(int kind, const double* prm, int mode, double tol,
 // adaptive ode12 / ode23 (material.cu k_adaptive on the host)
 #include "../../paper_2006_04391_b200/csrc/adaptive.cuh"
 
-template <int Scheme, bool Coupled>
-static int run_adaptive(const MichelSuquetLaw& L, const StepCtl& ctl, int64_t B, const double* eps_n,
+template <int Scheme, bool Coupled, class Law>
+static int run_adaptive(const Law& L, const StepCtl& ctl, int64_t B, const double* eps_n,
                         const double* a_n, const double* eps_np1, const double* dt, double* sig, double* a_out,
                         double* C, int32_t* sub, int32_t* rej, uint8_t* status) {
     int any = 0;
@@ -95,8 +103,8 @@ static int run_adaptive(const MichelSuquetLaw& L, const StepCtl& ctl, int64_t B,
                 stress_tangent(L, ep, an, nullptr, s2, Cv);
             }
         } else {
-            st = adaptive_point<MichelSuquetLaw, Scheme, Coupled>(L, ctl, en, an, ep, dt[b], a, da, s, r);
-            clamp_state<MichelSuquetLaw>(a, ac);
+            st = adaptive_point<Law, Scheme, Coupled>(L, ctl, en, an, ep, dt[b], a, da, s, r);
+            clamp_state<Law>(a, ac);
             if (Coupled) stress_tangent(L, ep, ac, da, sig + 6 * b, Cv);
             else stress_plain(L, ep, ac, sig + 6 * b);
         }
@@ -113,16 +121,20 @@ static int run_adaptive(const MichelSuquetLaw& L, const StepCtl& ctl, int64_t B,
 extern "C" int hostcheck_adaptive(const double* prm, int scheme, int coupled, int measure, double atol, double rtol,
                                   int max_sub, int64_t B, const double* eps_n, const double* a_n, const double* eps_np1,
                                   const double* dt, double* sig, double* a_out, double* C, int32_t* sub, int32_t* rej,
-                                  uint8_t* status) {
-    auto L = MichelSuquetLaw::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]);
+                                  uint8_t* status, int semi) {
     StepCtl ctl;
     ctl.atol = atol;
     ctl.rtol = rtol;
     ctl.max_substeps = max_sub;
     ctl.measure = measure;
-    if (scheme == 23)
-        return coupled ? run_adaptive<23, true>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status)
-                       : run_adaptive<23, false>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status);
-    return coupled ? run_adaptive<12, true>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status)
-                   : run_adaptive<12, false>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status);
+    auto go = [&](const auto& L) {
+        if (scheme == 23)
+            return coupled ? run_adaptive<23, true>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status)
+                           : run_adaptive<23, false>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej,
+                                                     status);
+        return coupled ? run_adaptive<12, true>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status)
+                       : run_adaptive<12, false>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status);
+    };
+    if (semi) return go(SemiLaw<MichelSuquetLaw>::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]));
+    return go(MichelSuquetLaw::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]));
 }

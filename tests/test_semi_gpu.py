@@ -1,0 +1,70 @@
+"""Semi-automatic strategy on the GPU vs the reference's semi-automatic
+results (tests/golden/material_semi.npz), and the basic scheme with it
+(identical 16^3 path iteration counts)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from _util import TOL_STATE, TOL_TANGENT, assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2006_04391_b200 import gsm
+    from paper_2006_04391_b200.evaluator import StrategyConfig, evaluate_arrays
+
+    return gsm, StrategyConfig, evaluate_arrays
+
+
+@pytest.mark.parametrize("tang", [False, True])
+def test_semi_implicit_euler(api, tang):
+    gsm, SC, ev = api
+    g = golden("material_semi.npz")
+    tag = f"ie_{'t' if tang else 'n'}"
+    cfg = SC(strategy="semi-automatic", integrator="implicit-euler")
+    r = ev(gsm.MichelSuquet(), cfg, g["eps_n"], g["a_n"], g["eps_np1"], g["dt"], want_tangent=tang)
+    assert np.array_equal(r.newton_iters, g[tag + "_iters"])
+    assert_close(r.sigma, g[tag + "_sigma"], TOL_STATE, "sigma")
+    assert_close(r.a, g[tag + "_a"], TOL_STATE, "a")
+    if tang:
+        assert_close(r.C, g[tag + "_C"], TOL_TANGENT, "C")
+
+
+@pytest.mark.parametrize("integ", ["ode12", "ode23"])
+@pytest.mark.parametrize("tang", [False, True])
+def test_semi_adaptive(api, integ, tang):
+    gsm, SC, ev = api
+    g = golden("material_semi.npz")
+    tag = f"{integ}_{'t' if tang else 'n'}"
+    cfg = SC(strategy="semi-automatic", integrator=integ)
+    r = ev(gsm.MichelSuquet(), cfg, g["eps_n"], g["a_n"], g["eps_np1"], g["dt"], want_tangent=tang)
+    assert np.array_equal(r.substeps, g[tag + "_substeps"])
+    assert np.array_equal(r.rejected, g[tag + "_rejected"])
+    assert_close(r.sigma, g[tag + "_sigma"], TOL_STATE, "sigma")
+    assert_close(r.a, g[tag + "_a"], TOL_STATE, "a")
+    if tang:
+        assert_close(r.C, g[tag + "_C"], TOL_TANGENT, "C")
+
+
+def test_semi_linear_elastic(api):
+    gsm, SC, ev = api
+    g = golden("material_semi.npz")
+    cfg = SC(strategy="semi-automatic", integrator="implicit-euler")
+    r = ev(gsm.LinearElastic(300e9, 0.25), cfg, g["eps_n"], np.zeros((256, 0)), g["eps_np1"], g["dt"], True)
+    assert_close(r.sigma, g["le_sigma"], 1e-15)
+    assert_close(r.C, g["le_C"], 1e-15)
+
+
+def test_semi_path16(api):
+    gsm, SC, _ = api
+    from paper_2006_04391_b200 import homogenize as H
+
+    g = golden("path16_conv.npz")
+    cfg = SC(strategy="semi-automatic", integrator="implicit-euler")
+    recs = H.run_loading_path(H.toy_mmc_grid(16), H.LoadingPath(steps=20), cfg)
+    assert [r["iterations"] for r in recs] == g["iterations"].tolist()
+    assert_close([r["sig"][0] for r in recs], g["sig"][:, 0], 1e-9)
+    assert_close([r["C11"] for r in recs], g["C11"], 1e-8)
