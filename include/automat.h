@@ -38,7 +38,8 @@ typedef enum am_status {
     AM_ERR_NCCL = 6,
     AM_ERR_ARG = 7,               /* ValueError on bad arguments */
     AM_ERR_NONFINITE = 8,         /* reference_update: non-finite tangent (homogenize.py:316-317) */
-    AM_ERR_INTEGRATION = 9        /* odeint.IntegrationError: substep cap / step underflow (odeint.py:30-31) */
+    AM_ERR_INTEGRATION = 9,       /* odeint.IntegrationError: substep cap / step underflow (odeint.py:30-31) */
+    AM_ERR_RADIAL = 10            /* gsm.NewtonError: conventional radial return stalled (gsm.py:40, 377-378) */
 } am_status;
 
 /* per-voxel status bits written by the material kernel */
@@ -46,6 +47,7 @@ typedef enum am_status {
 #define AM_VOXEL_SINGULAR 2u
 #define AM_VOXEL_NONFINITE 4u
 #define AM_VOXEL_INTEGRATION 8u
+#define AM_VOXEL_RADIAL 16u
 
 /* ---------------------------------------------------------------- laws
  * A law is its two potentials; the potentials live on the device.
@@ -64,8 +66,9 @@ typedef struct am_law {
 /* ---------------------------------------------------------------- config
  * StrategyConfig (evaluator.py:35-74).  Order of the enums follows
  * STRATEGIES / INTEGRATORS / ERROR_MEASURES (evaluator.py:26-28).  This
- * build implements strategy=automatic with the implicit-euler, ode12 and
- * ode23 integrators; other combinations return AM_ERR_CONFIG.
+ * build implements the automatic and semi-automatic strategies with the
+ * implicit-euler, ode12 and ode23 integrators and the conventional
+ * (radial return) implicit-Euler route; ode23s returns AM_ERR_CONFIG.
  */
 enum { AM_STRATEGY_CONVENTIONAL = 0, AM_STRATEGY_AUTOMATIC = 1, AM_STRATEGY_SEMI_AUTOMATIC = 2 };
 enum { AM_INTEGRATOR_IMPLICIT_EULER = 0, AM_INTEGRATOR_ODE12 = 1, AM_INTEGRATOR_ODE23 = 2, AM_INTEGRATOR_ODE23S = 3 };

@@ -24,6 +24,7 @@ AM_ERR_NCCL = 6
 AM_ERR_ARG = 7
 AM_ERR_NONFINITE = 8
 AM_ERR_INTEGRATION = 9
+AM_ERR_RADIAL = 10
 
 AM_LAW_LINEAR_ELASTIC = 0
 AM_LAW_MICHEL_SUQUET = 1
@@ -228,6 +229,10 @@ def check(rc, where=""):
         raise NewtonDivergenceError(msg)
     if rc == AM_ERR_INTEGRATION:
         raise IntegrationError(msg)
+    if rc == AM_ERR_RADIAL:
+        from .gsm import NewtonError
+
+        raise NewtonError(msg)
     if rc == AM_ERR_SINGULAR:
         raise SingularMatrixError(msg)
     if rc == AM_ERR_NOT_CONVERGED:

@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "adaptive.cuh"
+#include "conventional.cuh"
 #include "k1.cuh"
 #include "material.cuh"
 
@@ -180,11 +181,13 @@ int check_cfg(const am_cfg* cfg) {
     if (!cfg) return fail(AM_ERR_ARG, "cfg is NULL");
     const bool integ = cfg->integrator == AM_INTEGRATOR_IMPLICIT_EULER || cfg->integrator == AM_INTEGRATOR_ODE12 ||
                        cfg->integrator == AM_INTEGRATOR_ODE23;
-    const bool strat = cfg->strategy == AM_STRATEGY_AUTOMATIC || cfg->strategy == AM_STRATEGY_SEMI_AUTOMATIC;
+    const bool strat = cfg->strategy == AM_STRATEGY_AUTOMATIC || cfg->strategy == AM_STRATEGY_SEMI_AUTOMATIC ||
+                       (cfg->strategy == AM_STRATEGY_CONVENTIONAL && cfg->integrator == AM_INTEGRATOR_IMPLICIT_EULER);
     if (!strat || !integ)
         return fail(AM_ERR_CONFIG,
                     "the device implements the automatic and semi-automatic strategies with integrator "
-                    "implicit-euler, ode12 or ode23 (got strategy %d, integrator %d)",
+                    "implicit-euler, ode12 or ode23, and the conventional implicit-Euler route "
+                    "(got strategy %d, integrator %d)",
                     cfg->strategy, cfg->integrator);
     if (cfg->newton_mode != AM_NEWTON_INTERNAL && cfg->newton_mode != AM_NEWTON_STRESS)
         return fail(AM_ERR_CONFIG, "unknown newton mode %d", cfg->newton_mode);
@@ -280,6 +283,38 @@ __global__ void __launch_bounds__(128) k_adaptive(Law L, KArgs k) {
     }
 }
 
+// strategy="conventional" (evaluator.py:172-174): radial return of the
+// Michel-Suquet law; frozen points use the semi-automatic operations
+// (evaluator.py:128, 142-150)
+template <bool Tangent>
+__global__ void __launch_bounds__(128) k_conventional(SemiLaw<MichelSuquetLaw> S, KArgs k) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
+        const PointIO io(k, b);
+        double en[6], ep[6], an[7], a[7], sig[6], C[6][6];
+        io.eps(en, ep);
+        io.load_a<7>(k.a_n, an);
+        const double dt = io.dt();
+        int st = 0;
+        if (dt == 0.0) {
+            for (int i = 0; i < 7; ++i) a[i] = an[i];
+            stress_plain(S, ep, an, sig);
+            if (Tangent) S.Ce(C);
+        } else {
+            st = conventional_point(S, ep, an, dt, sig, a, Tangent ? C : nullptr);
+        }
+        if (Tangent) {
+            GlobalSink sink{k.C, k.lc.cs, b * k.lc.es};
+            put_all(sink, C);
+            if (!sink.finite) st |= ST_NONFINITE;
+        }
+        io.store_sigma(sig);
+        io.store_a<7>(a);
+        if (k.iters) k.iters[b] = 1;
+        if (k.rejected) k.rejected[b] = 0;
+        io.status(st);
+    }
+}
+
 template <class Law, int Scheme>
 static int launch_adaptive(const Law& L, const KArgs& k, unsigned g, cudaStream_t s) {
     if (k.C) k_adaptive<Law, Scheme, true><<<g, 128, 0, s>>>(L, k);
@@ -329,7 +364,17 @@ static int launch_law(const Law& L, KArgs k, cudaStream_t s) {
 
 int launch_material(const am_law* law, const KArgs& k, cudaStream_t s) {
     if (k.B == 0) return AM_OK;
-    const bool semi = k.strategy == AM_STRATEGY_SEMI_AUTOMATIC;
+    const bool semi = k.strategy == AM_STRATEGY_SEMI_AUTOMATIC || k.strategy == AM_STRATEGY_CONVENTIONAL;
+    if (law->kind == AM_LAW_MICHEL_SUQUET && k.strategy == AM_STRATEGY_CONVENTIONAL) {
+        const auto S = SemiLaw<MichelSuquetLaw>::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot,
+                                                      law->sigma_d, law->n);
+        int64_t blocks = (k.B + 127) / 128;
+        if (blocks > (int64_t)kSMs * 1024) blocks = (int64_t)kSMs * 1024;
+        if (k.C) k_conventional<true><<<(unsigned)blocks, 128, 0, s>>>(S, k);
+        else k_conventional<false><<<(unsigned)blocks, 128, 0, s>>>(S, k);
+        AM_CUDA(cudaGetLastError());
+        return AM_OK;
+    }
     if (law->kind == AM_LAW_MICHEL_SUQUET) {
         if (semi)
             return launch_law(SemiLaw<MichelSuquetLaw>::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot,
@@ -483,6 +528,7 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
         return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
     if (any & AM_VOXEL_INTEGRATION)
         return fail(AM_ERR_INTEGRATION, "adaptive integration: substep cap or step size underflow");
+    if (any & AM_VOXEL_RADIAL) return fail(AM_ERR_RADIAL, "radial return stalled");
     if (any & AM_VOXEL_SINGULAR) return fail(AM_ERR_SINGULAR, "pivot below 1e-14 * max|A|");
     return AM_OK;
 }

@@ -65,3 +65,16 @@ def adaptive(law, scheme, coupled, measure, eps_n, a_n, eps_np1, dt, atol=1e-6, 
         _p(sig), _p(a), _p(C), sub.ctypes.data_as(i32), rej.ctypes.data_as(i32),
         st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), int(bool(semi)))
     return dict(sigma=sig, a=a, C=C if coupled else None, substeps=sub, rejected=rej, status=st, code=code)
+
+
+def conventional(law, eps_np1, a_n, dt, want_tangent):
+    """Host build of the radial-return kernel (strategy='conventional')."""
+    kind, prm = law
+    eps_np1 = np.ascontiguousarray(eps_np1, dtype=float)
+    B = eps_np1.shape[0]
+    an = np.ascontiguousarray(a_n, dtype=float)
+    dt = np.ascontiguousarray(np.broadcast_to(np.asarray(dt, dtype=float), (B,)))
+    sig = np.zeros((B, 6)); a = np.zeros((B, 7)); C = np.zeros((B, 6, 6))
+    code = lib().hostcheck_conventional(_p(prm), ctypes.c_int64(B), _p(eps_np1), _p(an), _p(dt), int(bool(want_tangent)),
+                                        _p(sig), _p(a), _p(C))
+    return dict(sigma=sig, a=a, C=C if want_tangent else None, code=code)

@@ -267,6 +267,13 @@ def make_semi():
     le = gsm.LinearElastic(300e9, 0.25)
     r = evaluate_arrays(le, SEMI, en, np.zeros((256, 0)), ep, dt, want_tangent=True)
     out.update(le_sigma=r.sigma, le_C=r.C)
+    # conventional radial return (gsm.py:332-404, evaluator.py:172-174)
+    for tang in (False, True):
+        r = evaluate_arrays(law, CONV, en, an, ep, dt, want_tangent=tang)
+        tag = f"conv_{'t' if tang else 'n'}"
+        out[tag + "_sigma"], out[tag + "_a"] = r.sigma, r.a
+        if tang:
+            out[tag + "_C"] = r.C
     save("material_semi.npz", **out)
 
 

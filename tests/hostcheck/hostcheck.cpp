@@ -138,3 +138,25 @@ extern "C" int hostcheck_adaptive(const double* prm, int scheme, int coupled, in
     if (semi) return go(SemiLaw<MichelSuquetLaw>::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]));
     return go(MichelSuquetLaw::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]));
 }
+
+// conventional radial return (material.cu k_conventional on the host)
+#include "../../paper_2006_04391_b200/csrc/conventional.cuh"
+
+extern "C" int hostcheck_conventional(const double* prm, int64_t B, const double* eps_np1, const double* a_n,
+                                      const double* dt, int want_tangent, double* sig, double* a_out, double* C) {
+    auto S = SemiLaw<MichelSuquetLaw>::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]);
+    int any = 0;
+    for (int64_t b = 0; b < B; ++b) {
+        double Cv[6][6];
+        if (dt[b] == 0.0) {
+            std::memcpy(a_out + 7 * b, a_n + 7 * b, 7 * sizeof(double));
+            stress_plain(S, eps_np1 + 6 * b, a_n + 7 * b, sig + 6 * b);
+            S.Ce(Cv);
+        } else {
+            any |= conventional_point(S, eps_np1 + 6 * b, a_n + 7 * b, dt[b], sig + 6 * b, a_out + 7 * b,
+                                      want_tangent ? Cv : nullptr);
+        }
+        if (want_tangent) std::memcpy(C + 36 * b, Cv, sizeof(Cv));
+    }
+    return any;
+}

@@ -68,3 +68,26 @@ def test_semi_path16(api):
     assert [r["iterations"] for r in recs] == g["iterations"].tolist()
     assert_close([r["sig"][0] for r in recs], g["sig"][:, 0], 1e-9)
     assert_close([r["C11"] for r in recs], g["C11"], 1e-8)
+
+
+@pytest.mark.parametrize("tang", [False, True])
+def test_conventional(api, tang):
+    """strategy='conventional': radial return kernel vs the reference."""
+    gsm, SC, ev = api
+    g = golden("material_semi.npz")
+    tag = f"conv_{'t' if tang else 'n'}"
+    cfg = SC(strategy="conventional", integrator="implicit-euler")
+    r = ev(gsm.MichelSuquet(), cfg, g["eps_n"], g["a_n"], g["eps_np1"], g["dt"], want_tangent=tang)
+    assert_close(r.sigma, g[tag + "_sigma"], TOL_STATE, "sigma")
+    assert_close(r.a, g[tag + "_a"], TOL_STATE, "a")
+    if tang:
+        assert_close(r.C, g[tag + "_C"], TOL_TANGENT, "C")
+
+
+def test_conventional_rejects_linear_elastic(api):
+    gsm, SC, ev = api
+    from paper_2006_04391_b200.evaluator import ConfigError
+
+    cfg = SC(strategy="conventional", integrator="implicit-euler")
+    with pytest.raises(ConfigError):
+        ev(gsm.LinearElastic(1e9, 0.3), cfg, np.zeros((2, 6)), np.zeros((2, 0)), np.zeros((2, 6)), 0.1)

@@ -45,3 +45,15 @@ def test_semi_linear_elastic():
     r = HC.evaluate(OM.law_params(0, 300e9, 0.25), g["eps_n"], None, g["eps_np1"], g["dt"], True, semi=True)
     assert_close(r["sigma"], g["le_sigma"], 1e-15)
     assert_close(r["C"], g["le_C"], 1e-15)
+
+
+@pytest.mark.parametrize("tang", [False, True])
+def test_conventional(tang):
+    g = golden("material_semi.npz")
+    tag = f"conv_{'t' if tang else 'n'}"
+    r = HC.conventional(OM.ALUMINUM, g["eps_np1"], g["a_n"], g["dt"], tang)
+    assert r["code"] == 0
+    assert_close(r["sigma"], g[tag + "_sigma"], TOL_STATE, "sigma")
+    assert_close(r["a"], g[tag + "_a"], TOL_STATE, "a")
+    if tang:
+        assert_close(r["C"], g[tag + "_C"], TOL_TANGENT, "C")
