@@ -576,26 +576,35 @@ AM_HD double step_strain(const double* eps_n, const double* eps_np1, double dt, 
 // Mode: 0 internal / 1 stress convergence (odeint.py:388-395).
 // dt == 0 (frozen, evaluator.py:142-170): a = a_n, no iteration.
 template <class Law, int Mode>
-AM_HD int newton_point(const Law& L, const NewtonCfg& cfg, const double* eps_n, const double* a_n,
-                       const double* eps_np1, double dt, double* a, int& iters) {
-    constexpr int m = Law::m;
-    iters = 0;
+struct NewtonState {
+    static constexpr int m = Law::m;
+    static constexpr int ms = m > 0 ? m : 1;
+    double a0[ms], a[ms], e1[6], h, res_prev;
+    double sig_prev[Mode == 1 ? 6 : 1];
+    int growth, iters;
+
+    // MaterialStepProblem set-up; false when no iteration is needed
+    // (no state, or frozen dt == 0: a = a_n)
+    AM_HD bool init(const Law& L, const double* eps_n, const double* a_n, const double* eps_np1, double dt) {
+        iters = 0;
 #pragma unroll
-    for (int i = 0; i < m; ++i) a[i] = a_n[i];
-    if constexpr (m == 0) {
-        return 0;
-    } else {
-        if (dt == 0.0) return 0;
-        constexpr int nd = JacShape<Law>::nd;
-        const double h = dt;
-        double e1[6];
+        for (int i = 0; i < m; ++i) a0[i] = a[i] = a_n[i];
+        if (m == 0 || dt == 0.0) return false;
+        h = dt;
         step_strain(eps_n, eps_np1, dt, e1);
-        double res_prev = INFINITY;
-        int growth = 0;
-        const double tol2 = cfg.tol * cfg.tol;
-        double sig_prev[6];
+        res_prev = INFINITY;
+        growth = 0;
         if constexpr (Mode == 1) stress_plain(L, e1, a, sig_prev);
-        for (;;) {
+        return true;
+    }
+
+    // one iteration of _newton_implicit_euler (odeint.py:371-399):
+    // 0 = continue, 1 = converged, 2 = failed (odeint.py:397, 400)
+    AM_HD int step(const Law& L, const NewtonCfg& cfg) {
+        if constexpr (m == 0) {
+            return 1;
+        } else {
+            constexpr int nd = JacShape<Law>::nd;
             double f[m], J[m][nd], F[m], dl[m];
             rhs_jac_dense<Law, nd>(L, e1, a, f, J);
             SFact<m, nd> fac;
@@ -605,7 +614,7 @@ AM_HD int newton_point(const Law& L, const NewtonCfg& cfg, const double* eps_n, 
             bool finite = true;
 #pragma unroll
             for (int i = 0; i < m; ++i) {
-                F[i] = a[i] - a_n[i] - h * f[i];
+                F[i] = a[i] - a0[i] - h * f[i];
                 finite = finite && (F[i] - F[i] == 0.0);  // isfinite
                 dl[i] = F[i];
             }
@@ -643,15 +652,30 @@ AM_HD int newton_point(const Law& L, const NewtonCfg& cfg, const double* eps_n, 
             } else {
 #pragma unroll
                 for (int i = 0; i < m; ++i) sc[i] = dl[i] * frcp(1.0 + fabs(an[i]));
-                conv = msq<m>(sc) <= tol2;  // rms <= tol (odeint.py:395)
+                conv = msq<m>(sc) <= cfg.tol * cfg.tol;  // rms <= tol (odeint.py:395)
             }
 #pragma unroll
             for (int i = 0; i < m; ++i) a[i] = an[i];
-            if (bad || growth >= 5) return ST_NEWTON;  // odeint.py:397
-            if (conv) return 0;
-            if (iters >= cfg.max_it) return ST_NEWTON;  // iteration cap (odeint.py:400)
+            if (bad || growth >= 5) return 2;
+            if (conv) return 1;
+            if (iters >= cfg.max_it) return 2;
+            return 0;
         }
     }
+};
+
+template <class Law, int Mode>
+AM_HD int newton_point(const Law& L, const NewtonCfg& cfg, const double* eps_n, const double* a_n,
+                       const double* eps_np1, double dt, double* a, int& iters) {
+    NewtonState<Law, Mode> S;
+    int r = 1;
+    if (S.init(L, eps_n, a_n, eps_np1, dt))
+        while ((r = S.step(L, cfg)) == 0) {
+        }
+#pragma unroll
+    for (int i = 0; i < Law::m; ++i) a[i] = S.a[i];
+    iters = S.iters;
+    return r == 2 ? ST_NEWTON : 0;
 }
 
 // clamp_state (gsm.py:252-256): alpha >= 0; identity for laws without state
