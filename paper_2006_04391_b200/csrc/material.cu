@@ -15,126 +15,9 @@
 #include <mutex>
 #include <vector>
 
-#include "common.cuh"
-#include "adaptive.cuh"
-#include "conventional.cuh"
-#include "k1.cuh"
-#include "material.cuh"
+#include "k1_kernels.cuh"
 
 namespace am {
-
-// writes C[i][j] of item `off` to C[(i * 6 + j) * cs + off]
-struct GlobalSink {
-    double* C;
-    int64_t cs, off;
-    bool finite = true;
-    __device__ void col(int j, const double* c) {
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-            C[(i * 6 + j) * cs + off] = c[i];
-            finite = finite && (c[i] - c[i] == 0.0);
-        }
-    }
-};
-
-// K1: one thread per material point, grid-stride, all intermediates in
-// registers.  Two phases (material.cuh):
-//   k_material<Law, Mode, Raw>  Newton (+ clamp + stress unless Raw).  With
-//                               Raw the unclamped state goes to a_out for
-//                               the tangent phase.
-//   k_tangent<Law>              tangent post-process + clamp + stress + C.
-// Mode = Newton convergence measure; each combination is its own
-// instantiation so the hot Newton loop carries no dead code
-// (instruction-cache footprint).  The Newton kernel runs best at 3 CTAs per
-// SM (168 registers), the tangent kernel with the full 255-register budget
-// (tools/k1_variants.py measurements).
-#ifndef AM_K1_MINB_N
-#define AM_K1_MINB_N 3
-#endif
-#ifndef AM_K1_MINB_T
-#define AM_K1_MINB_T 1
-#endif
-
-struct PointIO {
-    const KArgs& k;
-    int64_t b, eo, ao;
-    __device__ PointIO(const KArgs& k_, int64_t b_) : k(k_), b(b_) {
-        const int64_t g = k.gidx ? k.gidx[b] : b;
-        eo = g * k.le.es;
-        ao = b * k.la.es;
-    }
-    __device__ void eps(double* en, double* ep) const {
-#pragma unroll
-        for (int c = 0; c < 6; ++c) {
-            en[c] = __ldg(k.eps_n + c * k.le.cs + eo);
-            ep[c] = __ldg(k.eps_np1 + c * k.le.cs + eo);
-        }
-    }
-    template <int m>
-    __device__ void load_a(const double* src, double* a) const {
-#pragma unroll
-        for (int c = 0; c < m; ++c) a[c] = src[c * k.la.cs + ao];
-    }
-    template <int m>
-    __device__ void store_a(const double* a) const {
-#pragma unroll
-        for (int c = 0; c < m; ++c) k.a_out[c * k.la.cs + ao] = a[c];
-    }
-    __device__ void store_sigma(const double* sig) const {
-#pragma unroll
-        for (int c = 0; c < 6; ++c) k.sigma[c * k.le.cs + eo] = sig[c];
-    }
-    __device__ double dt() const { return k.dt ? __ldg(k.dt + b) : k.dt_scalar; }
-    __device__ void status(int st) const {
-        if (k.status) k.status[b] = (uint8_t)st;
-        if (st && k.flags) atomicOr(k.flags, (uint32_t)st);
-    }
-};
-
-template <class Law, int Mode, bool Raw>
-__global__ void __launch_bounds__(128, AM_K1_MINB_N) k_material(Law L, KArgs k) {
-    constexpr int m = Law::m;
-    constexpr int ms = m > 0 ? m : 1;
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
-        const PointIO io(k, b);
-        double en[6], ep[6], an[ms], a[ms];
-        io.eps(en, ep);
-        io.load_a<m>(k.a_n, an);
-        int it = 0;
-        const int st = newton_point<Law, Mode>(L, k.ncfg, en, an, ep, io.dt(), a, it);
-        if constexpr (Raw) {
-            io.store_a<m>(a);
-        } else {
-            double ac[ms], sig[6];
-            stress_point(L, ep, a, ac, sig);
-            io.store_sigma(sig);
-            io.store_a<m>(ac);
-        }
-        if (k.iters) k.iters[b] = it;
-        io.status(st);
-    }
-}
-
-// reads the unclamped state from a_out and the Newton status from status
-template <class Law>
-__global__ void __launch_bounds__(128, AM_K1_MINB_T) k_tangent(Law L, KArgs k) {
-    constexpr int m = Law::m;
-    constexpr int ms = m > 0 ? m : 1;
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
-        const PointIO io(k, b);
-        double en[6], ep[6], a[ms], ac[ms], sig[6];
-        io.eps(en, ep);
-        if constexpr (m > 0) io.load_a<m>(k.a_out, a);
-        int st = (m > 0) ? k.status[b] : 0;
-        GlobalSink sink{k.C, k.lc.cs, b * k.lc.es};
-        if (st & ST_NEWTON) failed_point(L, ep, a, ac, sig, sink);
-        else st |= tangent_point(L, en, ep, io.dt(), a, ac, sig, sink);
-        if (!sink.finite) st |= ST_NONFINITE;
-        io.store_sigma(sig);
-        io.store_a<m>(ac);
-        io.status(st);
-    }
-}
 
 // gsm.py:574-602 at B points (AoS); used by the module-level API and the AD
 // unit tests.  eps dirs and a dirs are separate sweeps, like rhs_dual /
@@ -221,7 +104,7 @@ void set_controls(KArgs& k, const am_cfg* cfg) {
 // Stream-ordered scratch comes from the device's default memory pool; keep
 // freed blocks in the pool (release threshold = max) so per-call
 // allocations do not return memory to the driver at every synchronisation.
-static void keep_pool_memory() {
+void keep_pool_memory() {
     static std::mutex mu;
     static std::vector<int> done;
     int dev = 0;
@@ -236,155 +119,24 @@ static void keep_pool_memory() {
     done.push_back(dev);
 }
 
-// adaptive explicit integrators (odeint.py:636-756): one thread per point;
-// substeps -> iters, rejected attempts -> rejected.  Coupled = tangent.
-template <class Law, int Scheme, bool Coupled>
-__global__ void __launch_bounds__(128) k_adaptive(Law L, KArgs k) {
-    constexpr int m = Law::m;
-    constexpr int ms = m > 0 ? m : 1;
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
-        const PointIO io(k, b);
-        double en[6], ep[6], an[ms], a[ms], ac[ms], sig[6], da[ms][6];
-        io.eps(en, ep);
-        io.load_a<m>(k.a_n, an);
-        const double dt = io.dt();
-        int sub = 1, rej = 0, st = 0;
-        GlobalSink sink{k.C, k.lc.cs, b * k.lc.es};
-        if (dt == 0.0) {  // frozen (evaluator.py:142-150): a_n, elastic tangent, no clamp
-            for (int i = 0; i < m; ++i) ac[i] = an[i];
-            stress_plain(L, ep, an, sig);
-            if (Coupled) {
-                double C[6][6], s2[6];
-                stress_tangent(L, ep, an, nullptr, s2, C);
-                put_all(sink, C);
-            }
-        } else {
-            st = adaptive_point<Law, Scheme, Coupled>(L, k.sctl, en, an, ep, dt, a, da, sub, rej);
-            clamp_state<Law>(a, ac);  // evaluator.py:198
-            if (Coupled) {
-                double C[6][6];
-                stress_tangent(L, ep, ac, da, sig, C);  // evaluator.py:200
-                put_all(sink, C);
-            } else {
-                stress_plain(L, ep, ac, sig);
-            }
-        }
-        if (Coupled && !sink.finite) st |= ST_NONFINITE;
-        io.store_sigma(sig);
-        io.store_a<m>(ac);
-        if (k.iters) k.iters[b] = sub;
-        if (k.rejected) k.rejected[b] = rej;
-        if (k.sub_sum) {  // warp sum, one atomic per warp (integer: order independent)
-            const unsigned mask = __activemask();
-            const unsigned v = __reduce_add_sync(mask, (unsigned)sub);
-            if ((threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1)) atomicAdd(k.sub_sum, (unsigned long long)v);
-        }
-        io.status(st);
-    }
-}
-
-// strategy="conventional" (evaluator.py:172-174): radial return of the
-// Michel-Suquet law; frozen points use the semi-automatic operations
-// (evaluator.py:128, 142-150)
-template <bool Tangent>
-__global__ void __launch_bounds__(128) k_conventional(SemiLaw<MichelSuquetLaw> S, KArgs k) {
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
-        const PointIO io(k, b);
-        double en[6], ep[6], an[7], a[7], sig[6], C[6][6];
-        io.eps(en, ep);
-        io.load_a<7>(k.a_n, an);
-        const double dt = io.dt();
-        int st = 0;
-        if (dt == 0.0) {
-            for (int i = 0; i < 7; ++i) a[i] = an[i];
-            stress_plain(S, ep, an, sig);
-            if (Tangent) S.Ce(C);
-        } else {
-            st = conventional_point(S, ep, an, dt, sig, a, Tangent ? C : nullptr);
-        }
-        if (Tangent) {
-            GlobalSink sink{k.C, k.lc.cs, b * k.lc.es};
-            put_all(sink, C);
-            if (!sink.finite) st |= ST_NONFINITE;
-        }
-        io.store_sigma(sig);
-        io.store_a<7>(a);
-        if (k.iters) k.iters[b] = 1;
-        if (k.rejected) k.rejected[b] = 0;
-        io.status(st);
-    }
-}
-
-template <class Law, int Scheme>
-static int launch_adaptive(const Law& L, const KArgs& k, unsigned g, cudaStream_t s) {
-    if (k.C) k_adaptive<Law, Scheme, true><<<g, 128, 0, s>>>(L, k);
-    else k_adaptive<Law, Scheme, false><<<g, 128, 0, s>>>(L, k);
-    AM_CUDA(cudaGetLastError());
-    return AM_OK;
-}
-
-template <class Law>
-static int launch_law(const Law& L, KArgs k, cudaStream_t s) {
-    const int threads = 128;
-    int64_t blocks = (k.B + threads - 1) / threads;
-    if (blocks > (int64_t)kSMs * 1024) blocks = (int64_t)kSMs * 1024;
-    const unsigned g = (unsigned)blocks;
-    const bool stress = k.ncfg.mode == AM_NEWTON_STRESS;
-    if constexpr (Law::m > 0) {
-        if (k.integrator == AM_INTEGRATOR_ODE23) return launch_adaptive<Law, 23>(L, k, g, s);
-        if (k.integrator == AM_INTEGRATOR_ODE12) return launch_adaptive<Law, 12>(L, k, g, s);
-    }
-    if (!k.C) {
-        if (stress) k_material<Law, 1, false><<<g, threads, 0, s>>>(L, k);
-        else k_material<Law, 0, false><<<g, threads, 0, s>>>(L, k);
-        AM_CUDA(cudaGetLastError());
-        return AM_OK;
-    }
-    // tangent: Newton (raw state) then the tangent phase; the Newton status
-    // travels through `status` (a stream-ordered scratch when the caller
-    // does not want it)
-    uint8_t* scratch = nullptr;
-    if (Law::m > 0 && !k.status) {
-        keep_pool_memory();
-        AM_CUDA(cudaMallocAsync((void**)&scratch, (size_t)k.B, s));
-        k.status = scratch;
-    }
-    if (Law::m > 0) {
-        KArgs kn = k;
-        kn.flags = nullptr;  // the tangent kernel reports the combined status
-        if (stress) k_material<Law, 1, true><<<g, threads, 0, s>>>(L, kn);
-        else k_material<Law, 0, true><<<g, threads, 0, s>>>(L, kn);
-        AM_CUDA(cudaGetLastError());
-    }
-    k_tangent<Law><<<g, threads, 0, s>>>(L, k);
-    AM_CUDA(cudaGetLastError());
-    if (scratch) AM_CUDA(cudaFreeAsync(scratch, s));
-    return AM_OK;
-}
-
 int launch_material(const am_law* law, const KArgs& k, cudaStream_t s) {
     if (k.B == 0) return AM_OK;
     const bool semi = k.strategy == AM_STRATEGY_SEMI_AUTOMATIC || k.strategy == AM_STRATEGY_CONVENTIONAL;
     if (law->kind == AM_LAW_MICHEL_SUQUET && k.strategy == AM_STRATEGY_CONVENTIONAL) {
         const auto S = SemiLaw<MichelSuquetLaw>::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot,
                                                       law->sigma_d, law->n);
-        int64_t blocks = (k.B + 127) / 128;
-        if (blocks > (int64_t)kSMs * 1024) blocks = (int64_t)kSMs * 1024;
-        if (k.C) k_conventional<true><<<(unsigned)blocks, 128, 0, s>>>(S, k);
-        else k_conventional<false><<<(unsigned)blocks, 128, 0, s>>>(S, k);
-        AM_CUDA(cudaGetLastError());
-        return AM_OK;
+        return launch_conventional(S, k, s);
     }
     if (law->kind == AM_LAW_MICHEL_SUQUET) {
         if (semi)
-            return launch_law(SemiLaw<MichelSuquetLaw>::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot,
-                                                             law->sigma_d, law->n),
-                              k, s);
-        return launch_law(
+            return launch_law_ms_semi(SemiLaw<MichelSuquetLaw>::make(law->E, law->nu, law->sigma_Y, law->H,
+                                                                     law->eps0_dot, law->sigma_d, law->n),
+                                      k, s);
+        return launch_law_ms(
             MichelSuquetLaw::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot, law->sigma_d, law->n), k, s);
     }
-    if (semi) return launch_law(SemiLaw<LinearElasticLaw>::make(law->E, law->nu), k, s);
-    return launch_law(LinearElasticLaw::make(law->E, law->nu), k, s);
+    if (semi) return launch_law_le_semi(SemiLaw<LinearElasticLaw>::make(law->E, law->nu), k, s);
+    return launch_law_le(LinearElasticLaw::make(law->E, law->nu), k, s);
 }
 
 int law_m(const am_law* law) { return law->kind == AM_LAW_MICHEL_SUQUET ? 7 : 0; }
