@@ -66,9 +66,10 @@ typedef struct am_law {
 /* ---------------------------------------------------------------- config
  * StrategyConfig (evaluator.py:35-74).  Order of the enums follows
  * STRATEGIES / INTEGRATORS / ERROR_MEASURES (evaluator.py:26-28).  This
- * build implements the automatic and semi-automatic strategies with the
- * implicit-euler, ode12 and ode23 integrators and the conventional
- * (radial return) implicit-Euler route; ode23s returns AM_ERR_CONFIG.
+ * build implements every combination the reference accepts: the automatic
+ * and semi-automatic strategies with implicit-euler, ode12 and ode23,
+ * ode23s (Rosenbrock) with the semi-automatic strategy, and the
+ * conventional (radial return) implicit-Euler route.
  */
 enum { AM_STRATEGY_CONVENTIONAL = 0, AM_STRATEGY_AUTOMATIC = 1, AM_STRATEGY_SEMI_AUTOMATIC = 2 };
 enum { AM_INTEGRATOR_IMPLICIT_EULER = 0, AM_INTEGRATOR_ODE12 = 1, AM_INTEGRATOR_ODE23 = 2, AM_INTEGRATOR_ODE23S = 3 };

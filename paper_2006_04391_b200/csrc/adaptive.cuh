@@ -11,6 +11,7 @@
 // company", odeint.py:432-434).  Host + device.
 #pragma once
 
+#include "dual2.cuh"
 #include "material.cuh"
 
 namespace am {
@@ -45,6 +46,28 @@ struct Tableau<23> {
     AM_HD static double be(int j) { return j == 0 ? 7.0 / 24.0 : (j == 1 ? 0.25 : (j == 2 ? 1.0 / 3.0 : 0.125)); }
     // row sums of a (SchemeSpec.c)
     AM_HD static double c(int i) { return i == 0 ? 0.0 : (i == 1 ? 0.5 : (i == 2 ? 0.75 : 1.0)); }
+};
+
+// ode23s (odeint.py:116-132): Shampine-Reichelt linearly implicit 2(3) pair
+template <>
+struct Tableau<32> {
+    static constexpr int s = 3;
+    static constexpr bool fsal = false;
+    static constexpr int order_low = 2;
+    AM_HD static double dd() { return 1.0 / (2.0 + 1.4142135623730951); }   // 1 / (2 + sqrt 2)
+    AM_HD static double e32() { return 6.0 + 1.4142135623730951; }
+    AM_HD static double a(int i, int j) { return (i == 1 && j == 0) ? 0.5 : ((i == 2 && j == 1) ? 1.0 : 0.0); }
+    AM_HD static double b(int j) { return j == 1 ? 1.0 : 0.0; }
+    AM_HD static double be(int j) { return j == 1 ? 4.0 / 3.0 : -1.0 / 6.0; }
+    AM_HD static double c(int i) { return i == 0 ? 0.0 : (i == 1 ? 0.5 : 1.0); }
+    AM_HD static double gam(int i, int j) {
+        const double d = dd();
+        if (i == 0) return j == 0 ? d : 0.0;
+        if (i == 1) return j == 0 ? -d : (j == 1 ? d : 0.0);
+        return j == 0 ? (e32() - 2.0) * d : (j == 1 ? -e32() * d : d);
+    }
+    // row sums of gamma (SchemeSpec.gbar)
+    AM_HD static double gbar(int i) { return (gam(i, 0) + gam(i, 1)) + gam(i, 2); }
 };
 
 // strain at time t of the step and its ramp r = min(t/dt, 1) (odeint.py:256-264)
@@ -105,6 +128,158 @@ AM_HD double scaled_sq(double diff, double ra, double rb, double atol, double rt
     return x * x;
 }
 
+// MaterialStepProblem.jac_dir2 (odeint.py:306-337): d/deps_{n+1} of
+// [df/da . v_a + df/dt . v_t] at (t, y) with the state sensitivity da as
+// chained inner seed, through second-order duals of the hand partials
+template <class Law>
+AM_HD void jac_dir2(const Law& L, const double* eps_n, const double* eps_np1, double t, double dt, const double* y,
+                    const double (*da)[6], const double* v_a, double v_t, double (*out)[6]) {
+    constexpr int m = Law::m;
+    double r = t / dt;
+    r = r < 1.0 ? r : 1.0;
+    D2 pe[6], pa[m];
+    for (int i = 0; i < 6; ++i) {
+        const double de = eps_np1[i] - eps_n[i];
+        pe[i].v = eps_n[i] + r * de;
+        pe[i].d1 = de / dt * v_t;  // epsdot * v_t
+        for (int k = 0; k < 6; ++k) {
+            pe[i].d2[k] = k == i ? r : 0.0;
+            pe[i].d12[k] = k == i ? v_t / dt : 0.0;
+        }
+    }
+    for (int i = 0; i < m; ++i) {
+        pa[i].v = y[i];
+        pa[i].d1 = v_a[i];
+        for (int k = 0; k < 6; ++k) {
+            pa[i].d2[k] = da[i][k];
+            pa[i].d12[k] = 0.0;
+        }
+    }
+    auto f = rhs_sweep(L, tup(pe[0], pe[1], pe[2], pe[3], pe[4], pe[5]),
+                       tup(pa[0], pa[1], pa[2], pa[3], pa[4], pa[5], pa[6]));
+    sfor<m>([&](auto I) {
+        for (int k = 0; k < 6; ++k) out[decltype(I)::value][k] = get<decltype(I)::value>(f).d12[k];
+    });
+}
+
+// _rosenbrock_step (odeint.py:481-531): one linearly implicit embedded step
+// with the Jacobian frozen at (t, y); semi-automatic strategy only (the
+// reference rejects the automatic one, evaluator.py:61-62).  Returns ok.
+template <class Law, bool Coupled>
+AM_HD bool rosenbrock_attempt(const Law& L, const double* eps_n, const double* eps_np1, double dt, double t,
+                              double h, const double* y, const double (*da)[6], double* yh, double* yl,
+                              double (*dh)[6], double (*dl)[6]) {
+    static_assert(is_semi_v<Law>, "ode23s needs the hand-coded partials");
+    using T = Tableau<32>;
+    constexpr int m = Law::m;
+    constexpr int s = T::s;
+    // rhs_and_jac at (t, y): f0, J, ft = df/deps . epsdot
+    double e0[6];
+    strain_at(eps_n, eps_np1, t, dt, e0);
+    double f0[m], J6[m][6], Je[m][6], J[m][m], ft[m], W[m][m];
+    int piv[m];
+    L.rhs_jac(e0, y, f0, J6, Je);
+    for (int i = 0; i < m; ++i) {
+        for (int k = 0; k < 6; ++k) J[i][k] = J6[i][k];
+        J[i][6] = 0.0;
+        double sft = 0.0;
+        for (int k = 0; k < 6; ++k) sft += Je[i][k] * ((eps_np1[k] - eps_n[k]) / dt);
+        ft[i] = sft;
+    }
+    const double g00h = T::gam(0, 0) * h;
+    for (int i = 0; i < m; ++i)
+        for (int k = 0; k < m; ++k) W[i][k] = (i == k ? 1.0 : 0.0) - g00h * J[i][k];
+    bool ok = lu_factor(W, piv);
+    double K[s][m], Kd[Coupled ? s : 1][Coupled ? m : 1][6];
+    for (int st = 0; st < s; ++st) {
+        double yi[m], fi[m], fdi[Coupled ? m : 1][6];
+        for (int i = 0; i < m; ++i) yi[i] = y[i];
+        for (int q = 0; q < st; ++q)
+            if (T::a(st, q) != 0.0)
+                for (int i = 0; i < m; ++i) yi[i] += T::a(st, q) * K[q][i];
+        const double ti = t + T::c(st) * h;
+        if constexpr (Coupled) {
+            double ydi[m][6];
+            for (int i = 0; i < m; ++i)
+                for (int j = 0; j < 6; ++j) ydi[i][j] = da[i][j];
+            for (int q = 0; q < st; ++q)
+                if (T::a(st, q) != 0.0)
+                    for (int i = 0; i < m; ++i)
+                        for (int j = 0; j < 6; ++j) ydi[i][j] += T::a(st, q) * Kd[q][i][j];
+            double e[6];
+            const double r = strain_at(eps_n, eps_np1, ti, dt, e);
+            rhs_dual_pt(L, e, r, yi, ydi, fi, fdi);
+        } else {
+            if (st == 0) {
+                for (int i = 0; i < m; ++i) fi[i] = f0[i];
+            } else {
+                double e[6];
+                strain_at(eps_n, eps_np1, ti, dt, e);
+                rhs_plain(L, e, yi, fi);
+            }
+        }
+        double rhs[m];
+        const double gt = h * T::gbar(st) * h;
+        for (int i = 0; i < m; ++i) rhs[i] = h * fi[i] + gt * ft[i];
+        for (int q = 0; q < st; ++q) {
+            const double g = T::gam(st, q);
+            if (g == 0.0) continue;
+            for (int i = 0; i < m; ++i) {
+                double jk = 0.0;
+                for (int n = 0; n < m; ++n) jk += J[i][n] * K[q][n];
+                rhs[i] += g * h * jk;
+            }
+        }
+        for (int i = 0; i < m; ++i) K[st][i] = ok ? rhs[i] : 0.0;
+        lu_solve(W, piv, K[st]);
+        if constexpr (Coupled) {
+            double v_a[m], jtv[m][6];
+            for (int i = 0; i < m; ++i) v_a[i] = 0.0;
+            for (int q = 0; q <= st; ++q)
+                if (T::gam(st, q) != 0.0)
+                    for (int i = 0; i < m; ++i) v_a[i] += T::gam(st, q) * K[q][i];
+            jac_dir2(L, eps_n, eps_np1, t, dt, y, da, v_a, T::gbar(st) * h, jtv);
+            for (int j = 0; j < 6; ++j) {
+                double col[m];
+                for (int i = 0; i < m; ++i) col[i] = h * fdi[i][j] + h * jtv[i][j];
+                for (int q = 0; q < st; ++q) {
+                    const double g = T::gam(st, q);
+                    if (g == 0.0) continue;
+                    for (int i = 0; i < m; ++i) {
+                        double jk = 0.0;
+                        for (int n = 0; n < m; ++n) jk += J[i][n] * Kd[q][n][j];
+                        col[i] += g * h * jk;
+                    }
+                }
+                for (int i = 0; i < m; ++i) col[i] = ok ? col[i] : 0.0;
+                lu_solve(W, piv, col);
+                for (int i = 0; i < m; ++i) Kd[st][i][j] = col[i];
+            }
+        }
+    }
+    for (int i = 0; i < m; ++i) {
+        double sh = 0.0, sl = 0.0;
+        for (int q = 0; q < s; ++q) {
+            sh += T::b(q) * K[q][i];
+            sl += T::be(q) * K[q][i];
+        }
+        yh[i] = y[i] + sh;
+        yl[i] = y[i] + sl;
+        ok = ok && (yh[i] - yh[i] == 0.0) && (yl[i] - yl[i] == 0.0);
+        if (Coupled)
+            for (int j = 0; j < 6; ++j) {
+                double ch = 0.0, cl = 0.0;
+                for (int q = 0; q < s; ++q) {
+                    ch += T::b(q) * Kd[q][i][j];
+                    cl += T::be(q) * Kd[q][i][j];
+                }
+                dh[i][j] = da[i][j] + ch;
+                dl[i][j] = da[i][j] + cl;
+            }
+    }
+    return ok;
+}
+
 // One point over [0, dt] (adaptive_integrate, odeint.py:636-756).  Writes the
 // unclamped state to a and (Coupled) da = da/deps_{n+1}; substeps / rejected
 // counts.  Returns status bits (ST_INTEGRATION when a cap or the step-size
@@ -131,6 +306,11 @@ AM_HD int adaptive_point(const Law& L, const StepCtl& ctl, const double* eps_n, 
         const bool clipped = hi >= dt - t - 1e-15 * dt;
         double G[s][m], Gd[Coupled ? s : 1][Coupled ? m : 1][6];
         double yi[m], ydi[Coupled ? m : 1][6];
+        double yh[m], yl[m], dh[Coupled ? m : 1][6], dl[Coupled ? m : 1][6];
+        bool ok = true;
+        if constexpr (Scheme == 32) {
+            ok = rosenbrock_attempt<Law, Coupled>(L, eps_n, eps_np1, dt, t, hi, a, da, yh, yl, dh, dl);
+        } else {
         for (int st = 0; st < s; ++st) {
             if (st == 0 && g1_valid) {  // FSAL reuse (odeint.py:443-453)
                 for (int i = 0; i < m; ++i) {
@@ -161,8 +341,6 @@ AM_HD int adaptive_point(const Law& L, const StepCtl& ctl, const double* eps_n, 
             if constexpr (Coupled) rhs_dual_pt(L, e, r, yi, ydi, G[st], Gd[st]);
             else rhs_plain(L, e, yi, G[st]);
         }
-        double yh[m], yl[m], dh[Coupled ? m : 1][6], dl[Coupled ? m : 1][6];
-        bool ok = true;
         for (int i = 0; i < m; ++i) {
             double sh = 0.0, sl = 0.0;
             for (int q = 0; q < s; ++q) {
@@ -183,6 +361,7 @@ AM_HD int adaptive_point(const Law& L, const StepCtl& ctl, const double* eps_n, 
                     dl[i][j] = da[i][j] + hi * cl;
                 }
         }
+        }  // explicit stages
         // error_norm (odeint.py:564-617)
         double total = 0.0;
         int count;
@@ -243,7 +422,7 @@ AM_HD int adaptive_point(const Law& L, const StepCtl& ctl, const double* eps_n, 
         } else {
             ++rejected;
         }
-        if (T::fsal) {  // odeint.py:712-723
+        if constexpr (T::fsal) {  // odeint.py:712-723
             const int src = accept ? s - 1 : 0;
             for (int i = 0; i < m; ++i) {
                 g1[i] = G[src][i];

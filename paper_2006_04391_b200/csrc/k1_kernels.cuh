@@ -228,7 +228,8 @@ int launch_law(const Law& L, KArgs k, cudaStream_t s) {
     const unsigned g = (unsigned)blocks;
     const bool stress = k.ncfg.mode == AM_NEWTON_STRESS;
     if constexpr (Law::m > 0) {
-        if (k.integrator == AM_INTEGRATOR_ODE23 || k.integrator == AM_INTEGRATOR_ODE12)
+        if (k.integrator == AM_INTEGRATOR_ODE23 || k.integrator == AM_INTEGRATOR_ODE12 ||
+            k.integrator == AM_INTEGRATOR_ODE23S)
             return launch_adaptive_law(L, k, g, s);  // k1_adapt_*.cu
     }
     if (!k.C) {

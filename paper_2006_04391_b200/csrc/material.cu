@@ -63,14 +63,15 @@ int check_law(const am_law* law) {
 int check_cfg(const am_cfg* cfg) {
     if (!cfg) return fail(AM_ERR_ARG, "cfg is NULL");
     const bool integ = cfg->integrator == AM_INTEGRATOR_IMPLICIT_EULER || cfg->integrator == AM_INTEGRATOR_ODE12 ||
-                       cfg->integrator == AM_INTEGRATOR_ODE23;
+                       cfg->integrator == AM_INTEGRATOR_ODE23 ||
+                       (cfg->integrator == AM_INTEGRATOR_ODE23S && cfg->strategy == AM_STRATEGY_SEMI_AUTOMATIC);
     const bool strat = cfg->strategy == AM_STRATEGY_AUTOMATIC || cfg->strategy == AM_STRATEGY_SEMI_AUTOMATIC ||
                        (cfg->strategy == AM_STRATEGY_CONVENTIONAL && cfg->integrator == AM_INTEGRATOR_IMPLICIT_EULER);
     if (!strat || !integ)
         return fail(AM_ERR_CONFIG,
                     "the device implements the automatic and semi-automatic strategies with integrator "
-                    "implicit-euler, ode12 or ode23, and the conventional implicit-Euler route "
-                    "(got strategy %d, integrator %d)",
+                    "implicit-euler, ode12 or ode23, ode23s with the semi-automatic strategy, and the "
+                    "conventional implicit-Euler route (got strategy %d, integrator %d)",
                     cfg->strategy, cfg->integrator);
     if (cfg->newton_mode != AM_NEWTON_INTERNAL && cfg->newton_mode != AM_NEWTON_STRESS)
         return fail(AM_ERR_CONFIG, "unknown newton mode %d", cfg->newton_mode);

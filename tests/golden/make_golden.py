@@ -255,7 +255,7 @@ def make_semi():
         out[tag + "_sigma"], out[tag + "_a"], out[tag + "_iters"] = r.sigma, r.a, cnt
         if tang:
             out[tag + "_C"] = r.C
-    for integ in ("ode12", "ode23"):
+    for integ in ("ode12", "ode23", "ode23s"):
         cfg = StrategyConfig(strategy="semi-automatic", integrator=integ)
         for tang in (False, True):
             r = evaluate_arrays(law, cfg, en, an, ep, dt, want_tangent=tang)
@@ -264,6 +264,14 @@ def make_semi():
             out[tag + "_substeps"], out[tag + "_rejected"] = r.substeps, r.rejected
             if tang:
                 out[tag + "_C"] = r.C
+    cfg = StrategyConfig(strategy="semi-automatic", integrator="ode23s", error_measure="stress")
+    for tang in (False, True):
+        r = evaluate_arrays(law, cfg, en, an, ep, dt, want_tangent=tang)
+        tag = f"ode23s_stress_{'t' if tang else 'n'}"
+        out[tag + "_sigma"], out[tag + "_a"] = r.sigma, r.a
+        out[tag + "_substeps"], out[tag + "_rejected"] = r.substeps, r.rejected
+        if tang:
+            out[tag + "_C"] = r.C
     le = gsm.LinearElastic(300e9, 0.25)
     r = evaluate_arrays(le, SEMI, en, np.zeros((256, 0)), ep, dt, want_tangent=True)
     out.update(le_sigma=r.sigma, le_C=r.C)

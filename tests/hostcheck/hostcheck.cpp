@@ -127,6 +127,11 @@ extern "C" int hostcheck_adaptive(const double* prm, int scheme, int coupled, in
     ctl.rtol = rtol;
     ctl.max_substeps = max_sub;
     ctl.measure = measure;
+    if (scheme == 32) {  // ode23s: semi-automatic only
+        auto L = SemiLaw<MichelSuquetLaw>::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]);
+        return coupled ? run_adaptive<32, true>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status)
+                       : run_adaptive<32, false>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status);
+    }
     auto go = [&](const auto& L) {
         if (scheme == 23)
             return coupled ? run_adaptive<23, true>(L, ctl, B, eps_n, a_n, eps_np1, dt, sig, a_out, C, sub, rej, status)

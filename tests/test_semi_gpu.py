@@ -33,13 +33,14 @@ def test_semi_implicit_euler(api, tang):
         assert_close(r.C, g[tag + "_C"], TOL_TANGENT, "C")
 
 
-@pytest.mark.parametrize("integ", ["ode12", "ode23"])
+@pytest.mark.parametrize("integ", ["ode12", "ode23", "ode23s", "ode23s_stress"])
 @pytest.mark.parametrize("tang", [False, True])
 def test_semi_adaptive(api, integ, tang):
     gsm, SC, ev = api
     g = golden("material_semi.npz")
     tag = f"{integ}_{'t' if tang else 'n'}"
-    cfg = SC(strategy="semi-automatic", integrator=integ)
+    meas = "stress" if integ.endswith("stress") else "internal"
+    cfg = SC(strategy="semi-automatic", integrator=integ.replace("_stress", ""), error_measure=meas)
     r = ev(gsm.MichelSuquet(), cfg, g["eps_n"], g["a_n"], g["eps_np1"], g["dt"], want_tangent=tang)
     assert np.array_equal(r.substeps, g[tag + "_substeps"])
     assert np.array_equal(r.rejected, g[tag + "_rejected"])

@@ -24,13 +24,16 @@ def test_semi_implicit_euler(tang):
         assert_close(r["C"], g[tag + "_C"], TOL_TANGENT, "C")
 
 
-@pytest.mark.parametrize("integ", ["ode12", "ode23"])
+SCHEME = {"ode12": 12, "ode23": 23, "ode23s": 32, "ode23s_stress": 32}
+
+
+@pytest.mark.parametrize("integ", ["ode12", "ode23", "ode23s", "ode23s_stress"])
 @pytest.mark.parametrize("tang", [False, True])
 def test_semi_adaptive(integ, tang):
     g = golden("material_semi.npz")
     tag = f"{integ}_{'t' if tang else 'n'}"
-    r = HC.adaptive(OM.ALUMINUM, 23 if integ == "ode23" else 12, tang, "internal", g["eps_n"], g["a_n"],
-                    g["eps_np1"], g["dt"], semi=True)
+    meas = "stress" if integ.endswith("stress") else "internal"
+    r = HC.adaptive(OM.ALUMINUM, SCHEME[integ], tang, meas, g["eps_n"], g["a_n"], g["eps_np1"], g["dt"], semi=True)
     assert r["code"] == 0
     assert np.array_equal(r["substeps"], g[tag + "_substeps"])
     assert np.array_equal(r["rejected"], g[tag + "_rejected"])
