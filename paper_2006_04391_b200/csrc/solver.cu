@@ -112,7 +112,10 @@ __global__ void k_shift(double* __restrict__ eps, const double* __restrict__ eps
 // global origin.  Block b handles part (b % kParts) of ky plane (b / kParts);
 // its partial goes to red[(y0 + kyl) * kParts + part].
 // S: rfft(sigma) in, ehat'/N out;  ehat: rfft(eps) in, ehat' out.
-__global__ void __launch_bounds__(kRedThreads) k_fourier(Spec sp, RefMat ref, double2* __restrict__ S,
+#ifndef AM_FOURIER_MINB
+#define AM_FOURIER_MINB 1
+#endif
+__global__ void __launch_bounds__(kRedThreads, AM_FOURIER_MINB) k_fourier(Spec sp, RefMat ref, double2* __restrict__ S,
                                                          double2* __restrict__ ehat, double* __restrict__ red,
                                                          int update) {
     __shared__ double sh[kRedThreads / 32];

@@ -175,3 +175,33 @@ def test_odd_grid_vs_oracle(H, AUTO):
         ob.lam, ob.mu = OH.reference_update(oC)
         assert rel([hom.reference.lam, hom.reference.mu], [ob.lam, ob.mu]) < 1e-8
     assert rel(grid.state[0], ob.state[0]) < TOL
+
+
+def test_empty_phase_and_evaluate_field(H, AUTO):
+    """An unused material id, evaluate_field without tangent, free_mask None."""
+    from paper_2006_04391_b200 import gsm
+
+    ids = np.zeros((8, 6, 4), dtype=np.uint8)
+    ids[2:4] = 2
+    laws = [gsm.MichelSuquet(), gsm.LinearElastic(300e9, 0.25), gsm.LinearElastic(70e9, 0.3)]
+    grid = H.VoxelGrid(ids, laws)
+    hom = H.Homogenizer(grid, AUTO)
+    ob = OH.Basic(ids, [OM.ALUMINUM, OM.law_params(0, 300e9, 0.25), OM.law_params(0, 70e9, 0.3)])
+    assert rel([hom.reference.lam, hom.reference.mu], [ob.lam, ob.mu]) < 1e-14
+    eb = np.array([2e-3, 0, 0, 0, 0, 5e-4])
+    eps, sig, info = hom.solve_step(eb, 0.1)
+    oe, osig, oit, _ = ob.solve_step(eb, 0.1)
+    assert info.iterations == oit and rel(sig, osig) < TOL
+    s2, C, state, mean_sub = hom.evaluate_field(eps, 0.1)
+    assert C is None and mean_sub == 1.0 and rel(s2, sig) < 1e-15
+    assert state[1].shape == (0, 0) and state[0].shape == (len(grid.voxel_index[0]), 7)
+    hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+    assert rel(grid.state[0], ob.pending[0] if ob.pending is not None else ob.evaluate(oe, 0.1)[2][0]) < TOL
+
+
+def test_slab_count_must_divide(H, AUTO):
+    from paper_2006_04391_b200 import gsm
+
+    grid = H.VoxelGrid(np.zeros((6, 6, 4), dtype=np.uint8), [gsm.LinearElastic(1e9, 0.3)])
+    with pytest.raises(ValueError):
+        H.Homogenizer(grid, AUTO, slabs=4)

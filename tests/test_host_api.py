@@ -1,0 +1,86 @@
+"""Host-side parts of the drop-in API that need no GPU: geometry generation,
+loading path, geometry I/O, config validation, parameter files."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+
+def test_toy_mmc_grid_matches_reference_ids():
+    from paper_2006_04391_b200 import homogenize as H
+
+    assert np.array_equal(H.toy_mmc_grid(8).material_ids, golden("path8_auto.npz")["ids"])
+    assert np.array_equal(H.toy_mmc_grid(16).material_ids, golden("path16_conv.npz")["ids"])
+
+
+def test_sphere_ids_match_config1():
+    from paper_2006_04391_b200.workloads import sphere_ids
+
+    assert np.array_equal(sphere_ids(32), golden("config1.npz")["ids"])
+
+
+def test_loading_path_times_match_reference():
+    from paper_2006_04391_b200 import homogenize as H
+
+    g = golden("path16_conv.npz")
+    path = H.LoadingPath(steps=20)
+    t = path.times()
+    np.testing.assert_array_equal(t[1:], g["time"])
+    assert abs(path.total_time - 7.609635714285714) < 1e-12  # (2 eps_max - eps_min) / rate
+    assert path.eps_xx(t)[-1] == pytest.approx(-3.48441e-3)
+
+
+def test_voxel_grid_validation():
+    from paper_2006_04391_b200 import gsm, homogenize as H
+
+    with pytest.raises(ValueError):
+        H.VoxelGrid(np.zeros((4, 4)), [gsm.LinearElastic(1e9, 0.3)])
+    with pytest.raises(ValueError):
+        H.VoxelGrid(np.full((2, 2, 2), 3), [gsm.LinearElastic(1e9, 0.3)])
+    g = H.VoxelGrid(np.zeros((2, 3, 4), dtype=np.uint8), [gsm.MichelSuquet(), gsm.LinearElastic(1e9, 0.3)])
+    assert g.n_voxels == 24 and [len(i) for i in g.voxel_index] == [24, 0]
+    assert g.state[0].shape == (24, 7) and g.state[1].shape == (0, 0)
+
+
+def test_geometry_roundtrip(tmp_path):
+    from paper_2006_04391_b200 import homogenize as H
+
+    ids = H.toy_mmc_grid(8).material_ids
+    H.save_geometry(tmp_path / "g.raw", ids, ["matrix", "fiber"])
+    back, names = H.load_geometry(tmp_path / "g.raw")
+    assert np.array_equal(back, ids) and names == ["matrix", "fiber"]
+    big = np.full((2, 2, 2), 300)
+    H.save_geometry(tmp_path / "h.raw", big, ["x"] * 301)
+    assert H.load_geometry(tmp_path / "h.raw")[0].dtype == np.dtype("<u2")
+
+
+def test_strategy_config_validation():
+    from paper_2006_04391_b200.evaluator import ConfigError, StrategyConfig
+
+    assert StrategyConfig().integrator == "ode23"
+    assert StrategyConfig(error_measure="stress").resolved_newton_mode == "stress"
+    for bad in (dict(error_measure="x"), dict(newton_mode="y"), dict(integrator="rk4"),
+                dict(strategy="semi-automatic", integrator="ode23s", newton_mode="bad")):
+        with pytest.raises(ConfigError):
+            StrategyConfig(**bad)
+
+
+def test_michel_suquet_params_file(tmp_path):
+    from paper_2006_04391_b200 import gsm
+
+    p = tmp_path / "al.txt"
+    p.write_text("# aluminium\nE = 55e9\nnu = 0.33\nsigma_Y = 25e6\nH = 1.8e9\neps0_dot = 1\nsigma_d = 130e6\nn = 3.6\n")
+    assert gsm.load_michel_suquet_params(p) == gsm.ALUMINUM_MATRIX
+    p.write_text("E = 1\nbogus = 2\n")
+    with pytest.raises(ValueError):
+        gsm.load_michel_suquet_params(p)
+    with pytest.raises(ValueError):
+        gsm.MichelSuquetParams(E=1, nu=0.6, sigma_Y=1, H=1, eps0_dot=1, sigma_d=1, n=1)
+
+
+def test_reference_material_matrix():
+    from oracle import homogenize as OH
+    from paper_2006_04391_b200 import homogenize as H
+
+    np.testing.assert_array_equal(H.ReferenceMaterial(3.0, 2.0).matrix(), OH.iso_matrix(3.0, 2.0))
