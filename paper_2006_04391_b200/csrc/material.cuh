@@ -501,6 +501,34 @@ AM_HD auto da_block_tup(const double* a, const double (*da)[NJ], std::integer_se
     return tup(mk(I)...);
 }
 
+// stress_and_tangent columns J0 .. J0+NJ-1 at (eps_{n+1}, clamped a) seeded
+// (e_j, da[:, j]) (gsm.py:520-551; semi-automatic: C = d2w_ee + d2w_ae^T da)
+template <int J0, int NJ, class Law, class Sink>
+AM_HD void tangent_stress_block(const Law& L, const double* ac, const double* eps_np1, const double (*da)[NJ],
+                                double* sig, Sink& sink) {
+    constexpr int m = Law::m;
+    if constexpr (is_semi_v<Law>) {
+        sfor<NJ>([&](auto Jc) {
+            constexpr int jj = decltype(Jc)::value;
+            double c[6];
+            semi_stress_tangent_cols(L, eps_np1, ac, &da[0][jj], NJ, J0 + jj, sig, c);
+            sink.col(J0 + jj, c);
+        });
+        return;
+    }
+    auto s = stress_sweep(L, eps_seed_block<J0, NJ>(eps_np1, 1.0, seq<6>{}), da_block_tup<NJ>(ac, da, seq<m>{}));
+    sfor<NJ>([&](auto Jc) {
+        constexpr int jj = decltype(Jc)::value;
+        double c[6];
+        sfor<6>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            c[i] = get<i>(s).template dir<jj>();
+            sig[i] = get<i>(s).v;
+        });
+        sink.col(J0 + jj, c);
+    });
+}
+
 // Columns J0 .. J0+NJ-1 of the consistent tangent (odeint.py:417-426 then
 // gsm.py:520-551): df/deps_{n+1} for these strain directions (rhs_dual,
 // eps seeded r * e_j), (I - h J) da = 0 + h df/deps per column with the
@@ -524,26 +552,7 @@ AM_HD void tangent_block(const Law& L, const double* e1, double r, double h, con
 #pragma unroll
         for (int i = 0; i < m; ++i) da[i][jj] = x[i];
     });
-    if constexpr (is_semi_v<Law>) {
-        sfor<NJ>([&](auto Jc) {
-            constexpr int jj = decltype(Jc)::value;
-            double c[6];
-            semi_stress_tangent_cols(L, eps_np1, ac, &da[0][jj], NJ, J0 + jj, sig, c);
-            sink.col(J0 + jj, c);
-        });
-        return;
-    }
-    auto s = stress_sweep(L, eps_seed_block<J0, NJ>(eps_np1, 1.0, seq<6>{}), da_block_tup<NJ>(ac, da, seq<m>{}));
-    sfor<NJ>([&](auto Jc) {
-        constexpr int jj = decltype(Jc)::value;
-        double c[6];
-        sfor<6>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            c[i] = get<i>(s).template dir<jj>();
-            sig[i] = get<i>(s).v;
-        });
-        sink.col(J0 + jj, c);
-    });
+    tangent_stress_block<J0, NJ>(L, ac, eps_np1, da, sig, sink);
 }
 
 // ---------------------------------------------------------------- one point
@@ -726,6 +735,49 @@ AM_HD int tangent_point(const Law& L, const double* eps_n, const double* eps_np1
         double e1[6];
         const double r = step_strain(eps_n, eps_np1, dt, e1);
         int status = 0;
+#ifndef AM_TAN_BLOCK
+#define AM_TAN_BLOCK 6
+#endif
+#ifndef AM_TAN_COMBINED
+#define AM_TAN_COMBINED 1
+#endif
+        if constexpr (AM_TAN_COMBINED && !is_semi_v<Law>) {
+            // one sweep for the whole post-process: the state seeded with
+            // directions 0..m-1 (df/da, odeint.py:421) and eps_{n+1} with
+            // directions m..m+5 scaled by the ramp (rhs_dual, odeint.py:420)
+            static_assert(m + 6 <= kMaxDir, "too many directions");
+            auto fv = rhs_sweep(L, seed_tup<m>(e1, r, seq<6>{}), seed_tup<0>(a, 1.0, seq<m>{}));
+            double J[m][nd], dfp[m][6];
+            sfor<m>([&](auto I) {
+                constexpr int i = decltype(I)::value;
+                sfor<nd>([&](auto K) { J[i][decltype(K)::value] = get<i>(fv).template dir<decltype(K)::value>(); });
+                sfor<6>([&](auto K) { dfp[i][decltype(K)::value] = get<i>(fv).template dir<m + decltype(K)::value>(); });
+            });
+            SFact<m, nd> fac;
+            fac.build(J, h);
+            const bool fast = fac.factor();
+            if (!fast) {
+                double x[m];
+                for (int i = 0; i < m; ++i) x[i] = 0.0;
+                if (!exact_solve(L, e1, a, h, x, false, true)) status |= ST_SINGULAR;
+            }
+            sfor<6 / AM_TAN_BLOCK>([&](auto Bk) {
+                constexpr int J0 = decltype(Bk)::value * AM_TAN_BLOCK;
+                double da[m][AM_TAN_BLOCK];
+                sfor<AM_TAN_BLOCK>([&](auto Jc) {
+                    constexpr int jj = decltype(Jc)::value;
+                    double x[m];
+#pragma unroll
+                    for (int i = 0; i < m; ++i) x[i] = 0.0 + h * dfp[i][J0 + jj];
+                    if (fast) fac.solve(x);
+                    else exact_solve(L, e1, a, h, x, false, true);
+#pragma unroll
+                    for (int i = 0; i < m; ++i) da[i][jj] = x[i];
+                });
+                tangent_stress_block<J0, AM_TAN_BLOCK>(L, ac, eps_np1, da, sig, sink);
+            });
+            return status;
+        } else {
         double f[m], J[m][nd];
         rhs_jac_dense<Law, nd>(L, e1, a, f, J);
         SFact<m, nd> fac;
@@ -736,15 +788,13 @@ AM_HD int tangent_point(const Law& L, const double* eps_n, const double* eps_np1
             for (int i = 0; i < m; ++i) x[i] = 0.0;
             if (!exact_solve(L, e1, a, h, x, false, true)) status |= ST_SINGULAR;
         }
-#ifndef AM_TAN_BLOCK
-#define AM_TAN_BLOCK 2
-#endif
         // strain directions in blocks of AM_TAN_BLOCK columns
         sfor<6 / AM_TAN_BLOCK>([&](auto Bk) {
             tangent_block<decltype(Bk)::value * AM_TAN_BLOCK, AM_TAN_BLOCK>(L, e1, r, h, a, ac, eps_np1, fac, fast,
                                                                             sig, sink);
         });
         return status;
+        }
     }
 }
 
