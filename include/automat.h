@@ -181,6 +181,15 @@ int am_solver_create_slabs(int nx, int ny, int nz, const uint8_t *ids, int nmat,
 int am_nccl_unique_id(void *id128);
 int am_solver_create_nccl(int nx, int ny, int nz, const uint8_t *ids, int nmat, const am_law *laws,
                           const am_cfg *cfg, const void *id128, int rank, int nranks, am_solver **out);
+/* Fused transposes over NVLink for am_solver_create_nccl handles: export
+ * this rank's spectrum buffers (128 bytes of CUDA IPC handles), gather them
+ * from every rank (caller's transport, rank order) and import them; the
+ * forward transpose then packs straight into the peers' buffers and the
+ * inverse unpacks straight from them (one kernel each, no all-to-all).
+ * Handles from am_solver_create_slabs use the same kernels on their
+ * sibling slabs automatically. */
+int am_solver_ipc_export(am_solver *h, void *out128);
+int am_solver_ipc_import(am_solver *h, const void *all, int nranks);
 /* slab decomposition of a handle: global slab count, first local slab, local slabs */
 int am_solver_layout(am_solver *h, int *nslabs, int *first, int *nlocal);
 int am_solver_destroy(am_solver *h);

@@ -107,6 +107,8 @@ SIGNATURES = {
         ctypes.c_int, ctypes.c_int, ctypes.c_int, _u8p, ctypes.c_int, ctypes.POINTER(am_law), ctypes.POINTER(am_cfg),
         ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp),
     ]),
+    "am_solver_ipc_export": (ctypes.c_int, [_vp, ctypes.c_char_p]),
+    "am_solver_ipc_import": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int]),
     "am_solver_layout": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                         ctypes.POINTER(ctypes.c_int)]),
     "am_solver_destroy": (ctypes.c_int, [_vp]),

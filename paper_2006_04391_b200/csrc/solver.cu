@@ -224,6 +224,48 @@ __global__ void k_unpack(const double2* __restrict__ recv, double2* __restrict__
     }
 }
 
+// Fused transposes over peer memory (NVLink P2P / same-device siblings):
+// the pack kernel stores each destination's block straight into that
+// rank's spectrum buffer (dst[j] + rank * blk ...), so pack and all-to-all
+// are one pass; the inverse reads each source's block straight from that
+// rank's spectrum buffer.  `peer` is a device array of the k ranks' buffers.
+__global__ void k_pack_peer(const double2* __restrict__ P, double2* const* __restrict__ peer, int rank, int nxl, int ny,
+                            int nzh, int nyl) {
+    const int64_t blk = (int64_t)nxl * 6 * nyl * nzh;
+    const int64_t total = (int64_t)6 * nxl * ny * nzh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int kz = (int)(i % nzh);
+        int64_t r = i / nzh;
+        const int kyl = (int)(r % nyl);
+        r /= nyl;
+        const int c = (int)(r % 6);
+        r /= 6;
+        const int xl = (int)(r % nxl);
+        const int j = (int)(r / nxl);
+        const int ky = j * nyl + kyl;
+        peer[j][rank * blk + (i - j * blk)] = P[((int64_t)(c * nxl + xl) * ny + ky) * nzh + kz];
+    }
+    __threadfence_system();  // remote stores visible before the barrier that follows
+}
+
+__global__ void k_unpack_peer(double2* const* __restrict__ peer, double2* __restrict__ P, int rank, int nxl, int ny,
+                              int nzh, int nyl) {
+    const int64_t blk = (int64_t)nxl * 6 * nyl * nzh;
+    const int64_t total = (int64_t)6 * nxl * ny * nzh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int kz = (int)(i % nzh);
+        int64_t r = i / nzh;
+        const int kyl = (int)(r % nyl);
+        r /= nyl;
+        const int c = (int)(r % 6);
+        r /= 6;
+        const int xl = (int)(r % nxl);
+        const int src = (int)(r / nxl);
+        const int ky = src * nyl + kyl;
+        P[((int64_t)(c * nxl + xl) * ny + ky) * nzh + kz] = peer[src][rank * blk + (i - src * blk)];
+    }
+}
+
 // standalone Green application on a single-layout spectrum (GreenOperator.apply):
 // every bin, origin -> 0, output scaled by 1/N for the Z2D
 __global__ void k_green(Spec sp, RefMat ref, double2* __restrict__ h) {
@@ -407,6 +449,8 @@ struct Slab {
     double2 *P = nullptr, *X = nullptr;      // 2-D spectra / exchange buffer (multi-slab)
     uint32_t* flags = nullptr;
     unsigned long long* subs = nullptr;  // accepted substeps of the last sweep (adaptive integrators)
+    double2** peerS = nullptr;  // device arrays: every rank's S / ehat (P2P transport)
+    double2** peerE = nullptr;
     std::vector<Phase> phases;
 };
 
@@ -435,6 +479,8 @@ struct am_solver {
     double* stats = nullptr;
     double* hstats = nullptr;
     double* dsmall = nullptr;     // nccl reductions of the tangent statistics
+    bool p2p = false;             // fused pack / unpack over peer memory instead of the all-to-all
+    std::vector<void*> ipc_open;  // peer buffers opened with cudaIpcOpenMemHandle
     double lam = 0.0, mu = 0.0;
     double ebar_n[6] = {0, 0, 0, 0, 0, 0};
     bool pending = false;
@@ -458,6 +504,7 @@ static void solver_free(am_solver* h) {
         }
         cudaFree(s.eps); cudaFree(s.eps_n); cudaFree(s.sigma);
         cudaFree(s.S); cudaFree(s.ehat); cudaFree(s.P); cudaFree(s.X); cudaFree(s.flags); cudaFree(s.subs);
+        cudaFree(s.peerS); cudaFree(s.peerE);
     }
     cudaFree(h->red); cudaFreeHost(h->hred);
     cudaFree(h->Cbuf); cudaFree(h->status); cudaFree(h->stats); cudaFreeHost(h->hstats); cudaFree(h->dsmall);
@@ -465,6 +512,7 @@ static void solver_free(am_solver* h) {
         if (e) cudaEventDestroy(e);
     for (cufftHandle p : {h->r3, h->c3, h->r2, h->c2, h->x1})
         if (p) cufftDestroy(p);
+    for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
     if (h->comm) ncclCommDestroy(h->comm);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
@@ -501,12 +549,30 @@ static int reduce_to_host(am_solver* h, double* out) {
     return AM_OK;
 }
 
+// stream-ordered barrier across ranks (a 1-element all-reduce); in local
+// mode all slabs share one stream, which already orders them
+static int barrier(am_solver* h) {
+    if (h->comm) AM_NCCL(ncclAllReduce(h->dsmall + 63, h->dsmall + 63, 1, ncclDouble, ncclSum, h->comm, h->stream));
+    return AM_OK;
+}
+
 // ---------------------------------------------------------------- transforms
 // rfft of a real slab field -> spectrum buffer `dst` (S or ehat) of every slab
 static int forward(am_solver* h, double* Slab::*field, double2* Slab::*dst) {
     if (!h->multi) {
         Slab& s = h->slabs[0];
         AM_CUFFT(cufftExecD2Z(h->r3, s.*field, s.*dst));
+        return AM_OK;
+    }
+    if (h->p2p) {
+        for (auto& s : h->slabs) {
+            AM_CUFFT(cufftExecD2Z(h->r2, s.*field, s.P));
+            k_pack_peer<<<grid_for((int64_t)6 * s.nxl * h->ny * h->nzh), 256, 0, h->stream>>>(
+                s.P, dst == &Slab::S ? s.peerS : s.peerE, s.rank, s.nxl, h->ny, h->nzh, s.nyl);
+            AM_CUDA(cudaGetLastError());
+        }
+        AM_TRY(barrier(h));  // every block has landed
+        for (auto& s : h->slabs) AM_CUFFT(cufftExecZ2Z(h->x1, s.*dst, s.*dst, CUFFT_FORWARD));
         return AM_OK;
     }
     for (auto& s : h->slabs) {
@@ -528,6 +594,17 @@ static int inverse(am_solver* h, double2* Slab::*src, double* Slab::*field) {
         return AM_OK;
     }
     for (auto& s : h->slabs) AM_CUFFT(cufftExecZ2Z(h->x1, s.*src, s.*src, CUFFT_INVERSE));
+    if (h->p2p) {
+        AM_TRY(barrier(h));  // every rank's x-transform is done before it is read
+        for (auto& s : h->slabs) {
+            k_unpack_peer<<<grid_for((int64_t)6 * s.nxl * h->ny * h->nzh), 256, 0, h->stream>>>(
+                src == &Slab::S ? s.peerS : s.peerE, s.P, s.rank, s.nxl, h->ny, h->nzh, s.nyl);
+            AM_CUDA(cudaGetLastError());
+        }
+        AM_TRY(barrier(h));  // nobody overwrites a spectrum a peer is still reading
+        for (auto& s : h->slabs) AM_CUFFT(cufftExecZ2D(h->c2, s.P, s.*field));
+        return AM_OK;
+    }
     AM_TRY(alltoall(h, src, &Slab::X, (size_t)6 * h->slabs[0].nxl * h->slabs[0].nyl * h->nzh));
     for (auto& s : h->slabs) {
         k_unpack<<<grid_for((int64_t)6 * s.nxl * h->ny * h->nzh), 256, 0, h->stream>>>(s.X, s.P, s.nxl, h->ny,
@@ -697,6 +774,25 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
              plan(&h->x1, 1, n1, n1, bx, 1, n1, bx, 1, CUFFT_Z2Z, bx);
     }
     if (!ok) return bail(fail(AM_ERR_CUDA, "cufft plan creation failed for %dx%dx%d / %d slabs", nx, ny, nz, nslabs));
+    if (h->multi) {
+        for (auto& sl : h->slabs) {
+            if (cudaMalloc(&sl.peerS, sizeof(double2*) * nslabs) != cudaSuccess ||
+                cudaMalloc(&sl.peerE, sizeof(double2*) * nslabs) != cudaSuccess)
+                return bail(fail(AM_ERR_CUDA, "out of memory"));
+        }
+        if (!comm) {  // all slabs are local: the fused transposes address them directly
+            std::vector<double2*> S(nslabs), E(nslabs);
+            for (auto& sl : h->slabs) {
+                S[sl.rank] = sl.S;
+                E[sl.rank] = sl.ehat;
+            }
+            for (auto& sl : h->slabs)
+                if (cudaMemcpy(sl.peerS, S.data(), sizeof(double2*) * nslabs, cudaMemcpyHostToDevice) != cudaSuccess ||
+                    cudaMemcpy(sl.peerE, E.data(), sizeof(double2*) * nslabs, cudaMemcpyHostToDevice) != cudaSuccess)
+                    return bail(fail(AM_ERR_CUDA, "copy failed"));
+            h->p2p = true;
+        }
+    }
     *out = h;
     return AM_OK;
 }
@@ -727,6 +823,48 @@ extern "C" int am_solver_create_nccl(int nx, int ny, int nz, const uint8_t* ids,
     ncclComm_t comm = nullptr;
     AM_NCCL(ncclCommInitRank(&comm, nranks, id, rank));
     return solver_build(nx, ny, nz, ids, nmat, laws, cfg, nranks, rank, 1, comm, out);
+}
+
+// P2P transport for one-slab-per-process handles: export this rank's
+// spectrum buffers as CUDA IPC handles (2 x 64 bytes: S, ehat) ...
+extern "C" int am_solver_ipc_export(am_solver* h, void* out128) {
+    if (!h || !out128 || !h->comm) return fail(AM_ERR_ARG, "am_solver_ipc_export needs an nccl-mode handle");
+    AM_CUDA(cudaSetDevice(h->device));
+    cudaIpcMemHandle_t hs[2];
+    AM_CUDA(cudaIpcGetMemHandle(&hs[0], h->slabs[0].S));
+    AM_CUDA(cudaIpcGetMemHandle(&hs[1], h->slabs[0].ehat));
+    std::memcpy(out128, hs, sizeof(hs));
+    return AM_OK;
+}
+
+// ... and map every rank's (nranks x 128 bytes, rank order), switching the
+// transposes from ncclAlltoAll to the fused pack / unpack kernels over NVLink
+extern "C" int am_solver_ipc_import(am_solver* h, const void* all, int nranks) {
+    if (!h || !all || !h->comm || nranks != h->nslabs) return fail(AM_ERR_ARG, "am_solver_ipc_import: bad arguments");
+    AM_CUDA(cudaSetDevice(h->device));
+    Slab& sl = h->slabs[0];
+    std::vector<double2*> S(nranks), E(nranks);
+    const cudaIpcMemHandle_t* hs = (const cudaIpcMemHandle_t*)all;
+    for (int r = 0; r < nranks; ++r) {
+        if (r == sl.rank) {
+            S[r] = sl.S;
+            E[r] = sl.ehat;
+            continue;
+        }
+        void *ps = nullptr, *pe = nullptr;
+        AM_CUDA(cudaIpcOpenMemHandle(&ps, hs[2 * r], cudaIpcMemLazyEnablePeerAccess));
+        h->ipc_open.push_back(ps);
+        AM_CUDA(cudaIpcOpenMemHandle(&pe, hs[2 * r + 1], cudaIpcMemLazyEnablePeerAccess));
+        h->ipc_open.push_back(pe);
+        S[r] = (double2*)ps;
+        E[r] = (double2*)pe;
+    }
+    AM_CUDA(cudaMemcpy(sl.peerS, S.data(), sizeof(double2*) * nranks, cudaMemcpyHostToDevice));
+    AM_CUDA(cudaMemcpy(sl.peerE, E.data(), sizeof(double2*) * nranks, cudaMemcpyHostToDevice));
+    AM_CUDA(cudaMemsetAsync(h->dsmall, 0, sizeof(double) * 64, h->stream));
+    AM_CUDA(cudaStreamSynchronize(h->stream));
+    h->p2p = true;
+    return AM_OK;
 }
 
 extern "C" int am_solver_destroy(am_solver* h) {

@@ -9,17 +9,26 @@ batch.
 
 import ctypes
 from dataclasses import dataclass
+from typing import Callable, Optional
 
 from . import _lib
 
 
 @dataclass(frozen=True)
 class Comm:
-    """Rank, world size and the NCCL unique id of a communicator to create."""
+    """Rank, world size and the NCCL unique id of a communicator to create.
+
+    ``allgather`` (bytes -> list of every rank's bytes) lets the solver swap
+    CUDA IPC handles so the transposes run as fused pack / unpack kernels
+    over NVLink peer memory; ``transport`` = "p2p" (default when
+    ``allgather`` is given) or "nccl" (ncclAlltoAll).
+    """
 
     rank: int
     world: int
     uid: bytes
+    allgather: Optional[Callable[[bytes], list]] = None
+    transport: str = "p2p"
 
 
 def nccl_unique_id():
@@ -30,15 +39,22 @@ def nccl_unique_id():
     return buf.raw
 
 
-def comm_from_torch(group=None):
+def comm_from_torch(group=None, transport="p2p"):
     """Build a Comm over an initialised torch.distributed process group:
-    rank 0 creates the NCCL id, the group broadcasts it."""
+    rank 0 creates the NCCL id, the group broadcasts it (and later the IPC
+    handles of the P2P transport)."""
     import torch.distributed as dist
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
-    return Comm(rank=rank, world=world, uid=obj[0])
+
+    def allgather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b, group=group)
+        return out
+
+    return Comm(rank=rank, world=world, uid=obj[0], allgather=allgather, transport=transport)
 
 
 def slab_range(n, world, rank):

@@ -295,6 +295,12 @@ class Homogenizer:
             self._local_dims = tuple(grid.dims)
         _lib.check(rc, "Homogenizer")
         self._h = h
+        if comm is not None and comm.allgather is not None and comm.transport == "p2p":
+            # fused transposes over NVLink: swap the spectrum buffers' IPC handles
+            mine = ctypes.create_string_buffer(128)
+            _lib.check(self._lib.am_solver_ipc_export(h, mine), "ipc export")
+            every = comm.allgather(mine.raw)
+            _lib.check(self._lib.am_solver_ipc_import(h, b"".join(every), comm.world), "ipc import")
         self._ebar_n = np.zeros(6)
         self._last = None  # (eps, ebar) host arrays of the last converged step
         self._pending = False

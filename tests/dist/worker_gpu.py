@@ -21,7 +21,7 @@ def main():
     from paper_2006_04391_b200 import _lib
 
     _lib.check(_lib.load().am_set_device(local))
-    comm = D.comm_from_torch()
+    comm = D.comm_from_torch(transport=sys.argv[2] if len(sys.argv) > 2 else "p2p")
     cfg = StrategyConfig(strategy="automatic", integrator="implicit-euler")
     grid = H.toy_mmc_grid(16)
     hom = H.Homogenizer(grid, cfg, comm=comm)

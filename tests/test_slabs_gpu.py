@@ -91,8 +91,10 @@ def test_slabs_match_single_fields(mods):
         assert rel(st[0], st0[0]) < 1e-12
 
 
-def test_nccl_single_rank(mods, tmp_path):
-    """ncclAlltoAll / ncclAllReduce path (world 1) vs the local single-slab solver."""
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_nccl_single_rank(mods, tmp_path, transport):
+    """One slab per process (world 1 here): fused P2P transposes or
+    ncclAlltoAll, with ncclAllReduce reductions, vs the local single-slab solver."""
     gsm, H, cfg = mods
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -100,7 +102,7 @@ def test_nccl_single_rank(mods, tmp_path):
     out = tmp_path / "recs.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "dist", "worker_gpu.py"),
-           str(out)]
+           str(out), transport]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     got = json.load(open(out))
