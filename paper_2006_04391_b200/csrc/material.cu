@@ -168,11 +168,21 @@ extern "C" int am_eval_batch(const am_law* law, const am_cfg* cfg, int64_t B, co
 
 namespace {
 
-// Device staging for the host-pointer path: two slots so that chunk c+1's
-// copies overlap chunk c's kernel (the paper's two-stream staging,
-// PAPER.md:623, with device-resident buffers reused across calls).
+// Device staging for the host-pointer path: chunks of 2^17 points cycle
+// through three slots / streams so that the H2D copy of one chunk, the
+// kernels of another and the D2H copy of a third overlap (the paper's
+// two-stream staging, with device-resident buffers reused
+// across calls).  The path is PCIe-bound by the D2H of C (288 B/point);
+// 3 x 2^17 measured best (tools/e2e_variants.py: 8.67 ms per 2^20 vs
+// 9.0-9.2 ms for 2 x 2^18).
 struct HostPipe {
-    static constexpr int kSlots = 2;
+#ifndef AM_HOST_SLOTS
+#define AM_HOST_SLOTS 3
+#endif
+#ifndef AM_HOST_CHUNK_LOG2
+#define AM_HOST_CHUNK_LOG2 17
+#endif
+    static constexpr int kSlots = AM_HOST_SLOTS;
     int device = -1;
     int64_t cap = 0;
     cudaStream_t stream[kSlots] = {};
@@ -234,7 +244,7 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
         return fail(AM_ERR_ARG, "missing array argument");
     HostPipe& P = host_pipe();
     std::lock_guard<std::mutex> lock(P.mu);
-    const int64_t chunk = B < (int64_t(1) << 18) ? B : (int64_t(1) << 18);
+    const int64_t chunk = B < (int64_t(1) << AM_HOST_CHUNK_LOG2) ? B : (int64_t(1) << AM_HOST_CHUNK_LOG2);
     AM_TRY(P.ensure(chunk));
     AM_CUDA(cudaMemsetAsync(P.flags, 0, sizeof(uint32_t) * HostPipe::kSlots, P.stream[0]));
     AM_CUDA(cudaStreamSynchronize(P.stream[0]));

@@ -1,0 +1,44 @@
+"""e2e (host AoS arrays through am_eval_batch_host) timing of libautomat variants.
+usage (GPU box): python tools/e2e_variants.py"""
+import glob
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if len(sys.argv) > 1 and sys.argv[1] == "--one":
+    os.environ["AM_LIB"] = sys.argv[2]
+    sys.path.insert(0, ROOT)
+    import torch
+
+    from paper_2006_04391_b200 import _lib, gsm
+    from paper_2006_04391_b200.evaluator import StrategyConfig
+    from paper_2006_04391_b200.workloads import config2_batch
+
+    B = 1 << 20
+    lib = _lib.load()
+    law = _lib.make_law(gsm.MichelSuquet())
+    cfg = _lib.make_cfg(StrategyConfig(strategy="automatic", integrator="implicit-euler"))
+    en, an, ep, dt = config2_batch(B)
+    pin = lambda shape, dtype=torch.float64: torch.empty(shape, dtype=dtype, pin_memory=True).numpy()  # noqa: E731
+    h = [pin((B, 6)), pin((B, 7)), pin((B, 6)), pin((B,))]
+    h[0][:], h[1][:], h[2][:], h[3][:] = en, an, ep, dt
+    o = [pin((B, 6)), pin((B, 7)), pin((B, 6, 6)), pin((B,), torch.int32)]
+
+    def step():
+        _lib.check(lib.am_eval_batch_host(law, cfg, B, *[_lib.ptr(x) for x in h], 1, _lib.ptr(o[0]), _lib.ptr(o[1]),
+                                          _lib.ptr(o[2]), _lib.ptr(o[3], _lib._i32p), None, None))
+
+    for _ in range(2):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        step()
+    ms = (time.perf_counter() - t0) / 5 * 1e3
+    print(os.path.basename(os.path.dirname(sys.argv[2])), f"{ms:.3f} ms, {B / ms / 1e3:.3e} evals/s", flush=True)
+else:
+    libs = [os.path.join(ROOT, "paper_2006_04391_b200", "libautomat.so")]
+    libs += sorted(glob.glob(os.path.join(ROOT, "tools", "variants", "*", "libautomat.so")))
+    for lib in libs:
+        subprocess.run([sys.executable, __file__, "--one", lib], check=False)
