@@ -412,7 +412,7 @@ def main():
                      "work_per_launch": f"{fl:.4g} algorithmic fp64 flops per step (SURVEY §8d: 1072*N_it + 2273 per eval); "
                                     "one step = the Newton kernel + the tangent kernel"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "am_eval_batch_host (C ABI), pinned host AoS buffers, 2-stream chunked H2D|kernel|D2H"},
+                "path": "am_eval_batch_host (C ABI), pinned host AoS buffers, 3-stream chunked (2^17 points) H2D|kernels|D2H"},
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
     }
