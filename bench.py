@@ -173,7 +173,13 @@ def basic_scheme(n, lib, dev, dist=None):
     cfg = StrategyConfig(strategy="automatic", integrator="implicit-euler")
     grid = H.toy_mmc_grid(n)
     comm = D.comm_from_torch() if dist is not None else None
-    hom = H.Homogenizer(grid, cfg, comm=comm)
+    try:
+        hom = H.Homogenizer(grid, cfg, comm=comm)
+        ok = 1
+    except Exception as exc:  # noqa: BLE001 - reported in the JSON line
+        hom, ok, why = None, 0, f"{type(exc).__name__}: {exc}"
+    if not agree(dist, dev, ok):
+        return {"metric": "basic-scheme iterations/s", "error": why if not ok else "setup failed on another rank"}
     sp = ctypes.c_void_p()
     _lib.check(lib.am_solver_stream(hom._h, ctypes.byref(sp)))
     stream = torch.cuda.ExternalStream(sp.value, device=dev)
@@ -247,6 +253,18 @@ def loading_path_bench(n, dev, dist=None, steps=20):
                                    "reference update per step, run_loading_path (wall clock incl. tangent sweeps)"},
             "seconds": wall, "iterations_total": its, "iterations_per_step": [r["iterations"] for r in recs],
             "sig_xx_final": float(recs[-1]["sig"][0]), "C11_final": recs[-1]["C11"]}
+
+
+def agree(dist, dev, ok):
+    """All ranks proceed only if every rank's setup succeeded (no rank is left
+    waiting in a collective the others skipped)."""
+    if dist is None:
+        return bool(ok)
+    import torch
+
+    t = torch.tensor([int(ok)], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
 
 
 def hbm_peak():
@@ -387,8 +405,17 @@ def main():
     h2d = B * (6 + 7 + 6 + 1) * 8
     d2h = B * (6 + 7 + 36) * 8 + B * 4
     clocks = clk.summary()
-    basic = basic_scheme(args.basic, lib, dev, dist) if args.basic else None
-    path = loading_path_bench(args.path, dev, dist) if args.path else None
+    basic = path = None
+    if args.basic:
+        try:
+            basic = basic_scheme(args.basic, lib, dev, dist)
+        except Exception as exc:  # noqa: BLE001 - the headline line must still print
+            basic = {"metric": "basic-scheme iterations/s", "error": f"{type(exc).__name__}: {exc}"}
+    if args.path and (dist is None or "error" not in (basic or {})):
+        try:
+            path = loading_path_bench(args.path, dev, dist)
+        except Exception as exc:  # noqa: BLE001
+            path = {"metric": "basic-scheme iterations/s over the loading path", "error": f"{type(exc).__name__}: {exc}"}
 
     if rank != 0:
         if dist is not None:
