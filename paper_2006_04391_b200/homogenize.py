@@ -307,6 +307,8 @@ class Homogenizer:
         if comm is None:
             self._push_state(grid._state)
             grid._solver = self
+        else:
+            self._push_state(self._local_states(grid._state))
         self.reference = None
         self.set_reference(self.elastic_reference())
 
@@ -317,6 +319,18 @@ class Homogenizer:
             self._h = None
 
     # -- state transfer --------------------------------------------------------
+
+    def _local_states(self, states):
+        """This rank's part of per-phase global states (the voxels of its x-slab)."""
+        from .distributed import slab_range
+
+        x0, x1 = slab_range(self.grid.dims[0], self.comm.world, self.comm.rank)
+        plane = int(np.prod(self.grid.dims[1:]))
+        out = []
+        for arr, idx in zip(states, self.grid.voxel_index):
+            sel = (idx >= x0 * plane) & (idx < x1 * plane)
+            out.append(np.asarray(arr)[sel])
+        return out
 
     def _push_state(self, states):
         for i, (arr, law) in enumerate(zip(states, self.grid.materials)):
