@@ -182,3 +182,24 @@ def test_evaluate_batch_isolates_failures(api):
     assert list(errs) == [3] and errs[3].startswith("NewtonDivergenceError")
     for i in range(3):
         assert_close(res[i].sigma, g["large_n_sigma"][i], TOL_STATE)
+
+
+def test_evaluate_batch_groups_and_config_errors(api):
+    """material_ids grouping, a law without device potentials reported per
+    request, and batch results equal to single-request results."""
+    gsm, cfg, ev = api
+    from paper_2006_04391_b200.evaluator import EvalRequest, evaluate, evaluate_batch
+    from paper_2006_04391_b200.workloads import config2_batch
+
+    class PyLaw(gsm.GsmDefinition):
+        m = 0
+
+    en, an, ep, dt = config2_batch(6, seed=3)
+    reqs = [EvalRequest(en[i], an[i] if i % 3 else np.zeros(0), ep[i], 0.05, want_tangent=True) for i in range(6)]
+    ids = [1 if i % 3 else 0 for i in range(6)]
+    laws = {0: PyLaw(), 1: gsm.MichelSuquet()}
+    res, errs = evaluate_batch(laws, cfg, reqs, material_ids=ids)
+    assert sorted(errs) == [0, 3] and all(e.startswith("ConfigError") for e in errs.values())
+    for i in (1, 2, 4, 5):
+        one = evaluate(gsm.MichelSuquet(), cfg, reqs[i])
+        assert np.array_equal(res[i].sigma, one.sigma) and np.array_equal(res[i].C, one.C)
