@@ -132,6 +132,21 @@ int am_eval_batch_host(const am_law *law, const am_cfg *cfg, int64_t B,
                        int32_t *newton_iters, int32_t *rejected, uint8_t *status);
 
 /*
+ * am_eval_batch_record_host -- evaluate_arrays with record_steps=True for the
+ * adaptive integrators (EvalResult.steps, odeint.py:725-727): as
+ * am_eval_batch_host (host AoS arrays, one launch), plus every attempt's
+ * (step size, accepted) of point b at rec_h / rec_acc [offsets[b],
+ * offsets[b+1]).  offsets (B + 1 entries) are the prefix sums of the
+ * substeps + rejected counts of a previous evaluation of the same inputs
+ * (results are deterministic).
+ */
+int am_eval_batch_record_host(const am_law *law, const am_cfg *cfg, int64_t B,
+                              const double *eps_n, const double *a_n, const double *eps_np1,
+                              const double *dt, int want_tangent,
+                              double *sigma, double *a_out, double *C, int32_t *substeps, int32_t *rejected,
+                              const int64_t *offsets, double *rec_h, uint8_t *rec_acc);
+
+/*
  * am_constitutive_host -- module-level constitutive operations at B points
  * (gsm.stress / generalized_stress / evolution_rhs / rhs_jacobian /
  * rhs_strain_jacobian, gsm.py:574-602), evaluated by the same device AD

@@ -282,11 +282,12 @@ AM_HD bool rosenbrock_attempt(const Law& L, const double* eps_n, const double* e
 
 // One point over [0, dt] (adaptive_integrate, odeint.py:636-756).  Writes the
 // unclamped state to a and (Coupled) da = da/deps_{n+1}; substeps / rejected
-// counts.  Returns status bits (ST_INTEGRATION when a cap or the step-size
+// counts; with rec_h / rec_acc every attempt's step size and acceptance.  Returns status bits (ST_INTEGRATION when a cap or the step-size
 // underflow would raise IntegrationError).
 template <class Law, int Scheme, bool Coupled>
 AM_HD int adaptive_point(const Law& L, const StepCtl& ctl, const double* eps_n, const double* a_n,
-                         const double* eps_np1, double dt, double* a, double (*da)[6], int& substeps, int& rejected) {
+                         const double* eps_np1, double dt, double* a, double (*da)[6], int& substeps, int& rejected,
+                         double* rec_h = nullptr, uint8_t* rec_acc = nullptr) {
     using T = Tableau<Scheme>;
     constexpr int m = Law::m;
     constexpr int s = T::s;
@@ -410,6 +411,10 @@ AM_HD int adaptive_point(const Law& L, const StepCtl& ctl, const double* eps_n, 
         double err = sqrt(total / count);
         if (!(err - err == 0.0) || !ok) err = INFINITY;  // non-finite -> inf (odeint.py:617, 697)
         const bool accept = err <= 1.0;
+        if (rec_h) {  // record_steps: (attempted h, accepted) per attempt (odeint.py:725-727)
+            rec_h[substeps + rejected] = hi;
+            rec_acc[substeps + rejected] = accept ? 1 : 0;
+        }
         if (accept) {
             t = clipped ? dt : t + hi;
             for (int i = 0; i < m; ++i) {

@@ -37,6 +37,11 @@ struct KArgs {
     int strategy;       // AM_STRATEGY_*
     StepCtl sctl;
     unsigned long long* sub_sum;  // optional: += accepted substeps of the adaptive kernels
+    // optional step records of the adaptive kernels: point b's attempts at
+    // rec_h / rec_acc [rec_off[b], rec_off[b+1]) (record_steps)
+    const int64_t* rec_off;
+    double* rec_h;
+    uint8_t* rec_acc;
 };
 
 // validation and dispatch (material.cu)

@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(128) k_adaptive(Law L, KArgs k) {
                 put_all(sink, C);
             }
         } else {
-            st = adaptive_point<Law, Scheme, Coupled>(L, k.sctl, en, an, ep, dt, a, da, sub, rej);
+            double* rh = k.rec_h ? k.rec_h + k.rec_off[b] : nullptr;
+            uint8_t* ra = k.rec_h ? k.rec_acc + k.rec_off[b] : nullptr;
+            st = adaptive_point<Law, Scheme, Coupled>(L, k.sctl, en, an, ep, dt, a, da, sub, rej, rh, ra);
             clamp_state<Law>(a, ac);  // evaluator.py:198
             if (Coupled) {
                 double C[6][6];

@@ -296,6 +296,86 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
     return AM_OK;
 }
 
+// record_steps of the adaptive integrators: the same evaluation as
+// am_eval_batch_host (no chunking; meant for the reference's step-record
+// diagnostics), writing each point's attempts (step size, accepted) to
+// rec_h / rec_acc [offsets[b], offsets[b+1]); offsets (B + 1) come from the
+// substep + rejected counts of a previous evaluation of the same inputs.
+extern "C" int am_eval_batch_record_host(const am_law* law, const am_cfg* cfg, int64_t B, const double* eps_n,
+                                         const double* a_n, const double* eps_np1, const double* dt, int want_tangent,
+                                         double* sigma, double* a_out, double* C, int32_t* substeps,
+                                         int32_t* rejected, const int64_t* offsets, double* rec_h, uint8_t* rec_acc) {
+    AM_TRY(check_law(law));
+    AM_TRY(check_cfg(cfg));
+    if (B <= 0) return B == 0 ? AM_OK : fail(AM_ERR_ARG, "negative batch size");
+    const int m = law_m(law);
+    if (!eps_n || !eps_np1 || !dt || !sigma || !offsets || !rec_h || !rec_acc || (m && (!a_n || !a_out)) ||
+        (want_tangent && !C))
+        return fail(AM_ERR_ARG, "missing array argument");
+    const int64_t nrec = offsets[B];
+    std::vector<void*> bufs;
+    auto dalloc = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes ? bytes : 1) != cudaSuccess) return nullptr;
+        bufs.push_back(p);
+        return p;
+    };
+    auto cleanup = [&]() {
+        for (void* p : bufs) cudaFree(p);
+    };
+    double* d_in = (double*)dalloc(sizeof(double) * B * 20);
+    double* d_out = (double*)dalloc(sizeof(double) * B * 49);
+    int32_t* d_cnt = (int32_t*)dalloc(sizeof(int32_t) * B * 2);
+    uint8_t* d_st = (uint8_t*)dalloc(B);
+    int64_t* d_off = (int64_t*)dalloc(sizeof(int64_t) * (B + 1));
+    double* d_rh = (double*)dalloc(sizeof(double) * nrec);
+    uint8_t* d_ra = (uint8_t*)dalloc(nrec);
+    uint32_t* d_fl = (uint32_t*)dalloc(sizeof(uint32_t));
+    if (!d_in || !d_out || !d_cnt || !d_st || !d_off || !d_rh || !d_ra || !d_fl) {
+        cleanup();
+        return fail(AM_ERR_CUDA, "am_eval_batch_record_host: out of device memory");
+    }
+    double *d_en = d_in, *d_an = d_in + 6 * B, *d_e1 = d_in + 13 * B, *d_dt = d_in + 19 * B;
+    double *d_sig = d_out, *d_ao = d_out + 6 * B, *d_C = d_out + 13 * B;
+    cudaError_t e = cudaMemcpy(d_en, eps_n, sizeof(double) * 6 * B, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && m) e = cudaMemcpy(d_an, a_n, sizeof(double) * m * B, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_e1, eps_np1, sizeof(double) * 6 * B, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_dt, dt, sizeof(double) * B, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_off, offsets, sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(d_fl, 0, sizeof(uint32_t));
+    if (e != cudaSuccess) {
+        cleanup();
+        return fail(AM_ERR_CUDA, "am_eval_batch_record_host: %s", cudaGetErrorString(e));
+    }
+    KArgs k{};
+    k.B = B;
+    k.eps_n = d_en; k.a_n = d_an; k.eps_np1 = d_e1; k.dt = d_dt;
+    k.le = {1, 6}; k.la = {1, m}; k.lc = {1, 36};
+    k.sigma = d_sig; k.a_out = d_ao; k.C = want_tangent ? d_C : nullptr;
+    k.iters = d_cnt; k.rejected = d_cnt + B; k.status = d_st; k.flags = d_fl;
+    k.rec_off = d_off; k.rec_h = d_rh; k.rec_acc = d_ra;
+    set_controls(k, cfg);
+    int rc = launch_material(law, k, 0);
+    uint32_t any = 0;
+    if (rc == AM_OK) {
+        e = cudaMemcpy(sigma, d_sig, sizeof(double) * 6 * B, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && m) e = cudaMemcpy(a_out, d_ao, sizeof(double) * m * B, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && want_tangent) e = cudaMemcpy(C, d_C, sizeof(double) * 36 * B, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && substeps) e = cudaMemcpy(substeps, d_cnt, sizeof(int32_t) * B, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && rejected) e = cudaMemcpy(rejected, d_cnt + B, sizeof(int32_t) * B, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(rec_h, d_rh, sizeof(double) * nrec, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(rec_acc, d_ra, nrec, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(&any, d_fl, sizeof(any), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) rc = fail(AM_ERR_CUDA, "am_eval_batch_record_host: %s", cudaGetErrorString(e));
+    }
+    cleanup();
+    if (rc != AM_OK) return rc;
+    if (any & AM_VOXEL_NEWTON_FAILED) return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
+    if (any & AM_VOXEL_INTEGRATION) return fail(AM_ERR_INTEGRATION, "adaptive integration: substep cap");
+    if (any & AM_VOXEL_SINGULAR) return fail(AM_ERR_SINGULAR, "pivot below 1e-14 * max|A|");
+    return AM_OK;
+}
+
 extern "C" int am_constitutive_host(const am_law* law, int64_t B, const double* eps, const double* a,
                                     double* sigma, double* A, double* f, double* dfda, double* dfde) {
     AM_TRY(check_law(law));

@@ -199,6 +199,12 @@ def make_adaptive():
                 if tang:
                     out[tag + "_C"] = r.C
                 print(f"adaptive {tag}: {time.time() - t0:.1f}s, substeps {r.substeps.sum()}, rejected {r.rejected.sum()}")
+    # record_steps: every attempt's (h, accepted), including frozen points
+    cfg = StrategyConfig(strategy="automatic", integrator="ode23", record_steps=True)
+    r = evaluate_arrays(law, cfg, en[120:152], an[120:152], ep[120:152], dt[120:152], want_tangent=True)
+    flat = [(b, h, acc) for b, lst in enumerate(r.steps) for (h, acc) in lst]
+    out.update(rec_b=np.array([f[0] for f in flat]), rec_h=np.array([f[1] for f in flat]),
+               rec_acc=np.array([f[2] for f in flat]))
     # IntegrationError: substep cap on large increments
     cfg = StrategyConfig(strategy="automatic", integrator="ode23", max_substeps=3)
     e2 = np.zeros((4, 6))

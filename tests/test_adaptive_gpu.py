@@ -53,12 +53,18 @@ def test_integration_error(api):
         ev(gsm.MichelSuquet(), cfg, np.zeros((4, 6)), np.zeros((4, 7)), g["cap_eps_np1"], 1.0, want_tangent=True)
 
 
-def test_record_steps_rejected(api):
+def test_record_steps(api):
+    """EvalResult.steps of the adaptive integrator: every attempt's step size
+    (to round-off) and acceptance (exactly), frozen points [(0.0, True)]."""
     gsm, SC, ev = api
-    from paper_2006_04391_b200.evaluator import ConfigError
-
-    with pytest.raises(ConfigError):
-        ev(gsm.MichelSuquet(), SC(record_steps=True), np.zeros((2, 6)), np.zeros((2, 7)), np.zeros((2, 6)), 0.1)
+    g = golden("adaptive.npz")
+    cfg = SC(integrator="ode23", record_steps=True)
+    r = ev(gsm.MichelSuquet(), cfg, g["eps_n"][120:152], g["a_n"][120:152], g["eps_np1"][120:152], g["dt"][120:152],
+           want_tangent=True)
+    flat = [(b, h, acc) for b, lst in enumerate(r.steps) for (h, acc) in lst]
+    assert [f[0] for f in flat] == g["rec_b"].tolist()
+    assert [f[2] for f in flat] == g["rec_acc"].tolist()
+    np.testing.assert_allclose([f[1] for f in flat], g["rec_h"], rtol=1e-10, atol=0)
 
 
 def test_basic_scheme_with_ode23(api):
