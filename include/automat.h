@@ -256,6 +256,18 @@ int am_apply_isotropic_host(int64_t N, double lam, double mu, const double *eps,
 /* reference_update(C_field) (homogenize.py:307-329), C (n, 6, 6) */
 int am_reference_update_host(int64_t n, const double *C, double *lam, double *mu);
 
+/*
+ * am_lawops_host -- gsm.LawOps(law, strategy) (gsm.py:412-566) at B points:
+ * strategy AM_STRATEGY_AUTOMATIC (device AD) or SEMI_AUTOMATIC /
+ * CONVENTIONAL (hand partials, gsm.py:258-328; _ops_for maps conventional
+ * to semi-automatic, gsm.py:574-577).  AoS host arrays: eps (B,6), a (B,m),
+ * da (B,m,6) or NULL (frozen state: elastic tangent); outputs sigma (B,6),
+ * A (B,m), f (B,m), dfda (B,m,m), dfde (B,m,6), C (B,6,6), any NULL.
+ */
+int am_lawops_host(const am_law *law, int strategy, int64_t B, const double *eps, const double *a,
+                   const double *da, double *sigma, double *A, double *f, double *dfda, double *dfde,
+                   double *C);
+
 /* ---------------------------------------------------------------- diagnostics
  * am_probe_fp64_tflops -- sustained fp64 FMA throughput of the current
  * device (the roofline denominator of the material kernel; no reference

@@ -94,6 +94,9 @@ SIGNATURES = {
         _dp, _dp, _dp, _dp, ctypes.c_int, _dp, _dp, _dp, _i32p, _i32p, _i64p, _dp, _u8p,
     ]),
     "am_probe_fp64_tflops": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
+    "am_lawops_host": (ctypes.c_int, [
+        ctypes.POINTER(am_law), ctypes.c_int, ctypes.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+    ]),
     "am_constitutive_host": (ctypes.c_int, [
         ctypes.POINTER(am_law), ctypes.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
     ]),

@@ -52,6 +52,59 @@ __global__ void k_constitutive(Law L, int64_t B, const double* eps, const double
     }
 }
 
+// LawOps (gsm.py:412-566) at B points for either strategy: sigma, A, f,
+// df/da, df/deps (rhs_and_jacobians, gsm.py:488-518; semi-automatic:
+// rhs_jac_generic, gsm.py:463-481) and, with da (B, m, 6), the consistent
+// tangent C = stress_and_tangent (gsm.py:520-551); all AoS, any output NULL.
+template <class Law>
+__global__ void k_lawops(Law L, int64_t B, const double* eps, const double* a, const double* da, double* sigma,
+                         double* A, double* f, double* dfda, double* dfde, double* C) {
+    constexpr int m = Law::m;
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double e[6], s[6], av[m > 0 ? m : 1];
+    for (int c = 0; c < 6; ++c) e[c] = eps[6 * b + c];
+    for (int c = 0; c < m; ++c) av[c] = a[m * b + c];
+    stress_plain(L, e, av, s);
+    if (sigma)
+        for (int c = 0; c < 6; ++c) sigma[6 * b + c] = s[c];
+    if (C) {
+        double Cv[6][6], s2[6], dav[m > 0 ? m : 1][6];
+        for (int k = 0; k < m; ++k)
+            for (int j = 0; j < 6; ++j) dav[k][j] = da ? da[(m * b + k) * 6 + j] : 0.0;
+        stress_tangent(L, e, av, (m && da) ? dav : nullptr, s2, Cv);
+        for (int i = 0; i < 6; ++i)
+            for (int j = 0; j < 6; ++j) C[36 * b + 6 * i + j] = Cv[i][j];
+    }
+    if constexpr (m > 0) {
+        if (A) {
+            auto Av = gen_stress_sweep(L, plain_tup<6>(e, seq<6>{}), plain_tup<m>(av, seq<m>{}));
+            sfor<m>([&](auto I) { A[m * b + decltype(I)::value] = get<decltype(I)::value>(Av).v; });
+        }
+        if (f || dfda || dfde) {
+            double fv[m], J[m][m], Je[m][6];
+            if constexpr (is_semi_v<Law>) {
+                double J6[m][6];
+                L.rhs_jac(e, av, fv, J6, Je);
+                for (int i = 0; i < m; ++i) {
+                    for (int k = 0; k < 6; ++k) J[i][k] = J6[i][k];
+                    J[i][6] = 0.0;
+                }
+            } else {
+                rhs_jac_a(L, e, av, fv, J);
+                rhs_jac_eps(L, e, 1.0, av, Je);
+            }
+            for (int i = 0; i < m; ++i) {
+                if (f) f[m * b + i] = fv[i];
+                for (int k = 0; k < m; ++k)
+                    if (dfda) dfda[(m * b + i) * m + k] = J[i][k];
+                for (int k = 0; k < 6; ++k)
+                    if (dfde) dfde[(m * b + i) * 6 + k] = Je[i][k];
+            }
+        }
+    }
+}
+
 int check_law(const am_law* law) {
     if (!law) return fail(AM_ERR_ARG, "law is NULL");
     if (law->kind != AM_LAW_LINEAR_ELASTIC && law->kind != AM_LAW_MICHEL_SUQUET)
@@ -374,6 +427,52 @@ extern "C" int am_eval_batch_record_host(const am_law* law, const am_cfg* cfg, i
     if (any & AM_VOXEL_INTEGRATION) return fail(AM_ERR_INTEGRATION, "adaptive integration: substep cap");
     if (any & AM_VOXEL_SINGULAR) return fail(AM_ERR_SINGULAR, "pivot below 1e-14 * max|A|");
     return AM_OK;
+}
+
+extern "C" int am_lawops_host(const am_law* law, int strategy, int64_t B, const double* eps, const double* a,
+                              const double* da, double* sigma, double* A, double* f, double* dfda, double* dfde,
+                              double* C) {
+    AM_TRY(check_law(law));
+    if (strategy != AM_STRATEGY_AUTOMATIC && strategy != AM_STRATEGY_SEMI_AUTOMATIC &&
+        strategy != AM_STRATEGY_CONVENTIONAL)
+        return fail(AM_ERR_CONFIG, "unsupported strategy %d", strategy);
+    if (B <= 0) return B == 0 ? AM_OK : fail(AM_ERR_ARG, "negative batch size");
+    const int m = law_m(law);
+    const bool semi = strategy != AM_STRATEGY_AUTOMATIC;  // _ops_for: conventional -> semi-automatic
+    const size_t sz[] = {6, (size_t)m, (size_t)m * 6, 6, (size_t)m, (size_t)m, (size_t)m * m, (size_t)m * 6, 36};
+    const double* hin[] = {eps, a, da};
+    double* hout[] = {sigma, A, f, dfda, dfde, C};
+    std::vector<double*> d(9, nullptr);
+    int rc = AM_OK;
+    for (int i = 0; i < 9 && rc == AM_OK; ++i) {
+        const bool want = i < 3 ? hin[i] != nullptr : hout[i - 3] != nullptr;
+        if (want && sz[i] && cudaMalloc(&d[i], sizeof(double) * sz[i] * B) != cudaSuccess)
+            rc = fail(AM_ERR_CUDA, "am_lawops_host: out of memory");
+        if (rc == AM_OK && i < 3 && d[i] &&
+            cudaMemcpy(d[i], hin[i], sizeof(double) * sz[i] * B, cudaMemcpyHostToDevice) != cudaSuccess)
+            rc = fail(AM_ERR_CUDA, "am_lawops_host: copy failed");
+    }
+    if (rc == AM_OK) {
+        const unsigned blocks = unsigned((B + 127) / 128);
+        auto go = [&](const auto& L) {
+            k_lawops<<<blocks, 128>>>(L, B, d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8]);
+        };
+        if (law->kind == AM_LAW_MICHEL_SUQUET) {
+            if (semi)
+                go(SemiLaw<MichelSuquetLaw>::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot, law->sigma_d,
+                                                  law->n));
+            else go(MichelSuquetLaw::make(law->E, law->nu, law->sigma_Y, law->H, law->eps0_dot, law->sigma_d, law->n));
+        } else {
+            if (semi) go(SemiLaw<LinearElasticLaw>::make(law->E, law->nu));
+            else go(LinearElasticLaw::make(law->E, law->nu));
+        }
+        if (cudaGetLastError() != cudaSuccess) rc = fail(AM_ERR_CUDA, "am_lawops_host: launch failed");
+    }
+    for (int i = 3; i < 9 && rc == AM_OK; ++i)
+        if (d[i] && cudaMemcpy(hout[i - 3], d[i], sizeof(double) * sz[i] * B, cudaMemcpyDeviceToHost) != cudaSuccess)
+            rc = fail(AM_ERR_CUDA, "am_lawops_host: kernel failed");
+    for (double* p : d) cudaFree(p);
+    return rc;
 }
 
 extern "C" int am_constitutive_host(const am_law* law, int64_t B, const double* eps, const double* a,

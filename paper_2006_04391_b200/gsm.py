@@ -12,7 +12,9 @@ same formulas the device code compiles, usable for inspection on plain
 floats).
 
 Module-level operations (``stress`` ... ``rhs_strain_jacobian``,
-gsm.py:574-602) run on the GPU through ``am_constitutive_host``.
+gsm.py:574-602) and ``LawOps`` (gsm.py:412-566) run on the GPU through
+``am_lawops_host``; ``conventional_evaluate`` through the conventional route
+of ``am_eval_batch_host``.
 """
 
 from dataclasses import dataclass
@@ -201,6 +203,10 @@ class MichelSuquet(GsmDefinition):
         out[..., 6] = np.maximum(out[..., 6], 0.0)
         return out
 
+    def conventional_step(self, eps_n, a_n, eps_np1, h, want_tangent):
+        """Backward-Euler radial return, ``(sigma, a_new, C)`` (gsm.py:332-404), on the device."""
+        return _conventional_step(self, eps_n, a_n, eps_np1, h, want_tangent)
+
     @property
     def d2w_ee(self):
         return self.Ce
@@ -218,12 +224,15 @@ class MichelSuquet(GsmDefinition):
 # module-level constitutive operations (gsm.py:574-602), on the device
 # ---------------------------------------------------------------------------
 
-_STRATEGIES = ("automatic", "semi-automatic", "conventional")
+_STRATEGY_CODES = {"automatic": 1, "semi-automatic": 2, "conventional": 0}
 
 
-def _constitutive(law, eps, a, strategy):
-    if strategy not in _STRATEGIES:
+def _lawops(law, strategy, eps, a, da=None, want=("sigma", "A", "f", "dfda", "dfde"), C=False):
+    """One device call of LawOps at arbitrary leading batch shape (gsm.py:412-418)."""
+    if strategy not in _STRATEGY_CODES:
         raise ValueError(f"unsupported strategy {strategy!r}")
+    if strategy in ("semi-automatic", "conventional") and not law.has_hand_partials:
+        raise ValueError("law does not ship hand-coded partials")  # _ops_for maps conventional to semi (gsm.py:574-577)
     lib = _lib.load()
     s_law = _lib.make_law(law)
     m = law.m
@@ -232,38 +241,124 @@ def _constitutive(law, eps, a, strategy):
     B = int(np.prod(batch, dtype=np.int64))
     e = _lib.f64(eps, (B, 6))
     av = _lib.f64(np.broadcast_to(np.asarray(a, dtype=float), batch + (m,)), (B, m)) if m else np.zeros((B, 1))
-    sig = np.zeros((B, 6))
-    A = np.zeros((B, max(m, 1)))
-    f = np.zeros((B, max(m, 1)))
-    J = np.zeros((B, max(m, 1), max(m, 1)))
-    Je = np.zeros((B, max(m, 1), 6))
-    rc = lib.am_constitutive_host(s_law, B, _lib.ptr(e), _lib.ptr(av), _lib.ptr(sig), _lib.ptr(A), _lib.ptr(f),
-                                  _lib.ptr(J), _lib.ptr(Je))
-    _lib.check(rc, "constitutive")
-    return (sig.reshape(batch + (6,)), A[:, :m].reshape(batch + (m,)), f[:, :m].reshape(batch + (m,)),
-            J[:, :m, :m].reshape(batch + (m, m)), Je[:, :m].reshape(batch + (m, 6)))
+    dav = _lib.f64(np.broadcast_to(np.asarray(da, dtype=float), batch + (m, 6)), (B, m, 6)) if (da is not None and m) \
+        else None
+    mm = max(m, 1)
+    out = {"sigma": np.zeros((B, 6)), "A": np.zeros((B, mm)), "f": np.zeros((B, mm)), "dfda": np.zeros((B, mm, mm)),
+           "dfde": np.zeros((B, mm, 6))}
+    Cv = np.zeros((B, 6, 6)) if C else None
+    ptr = {k: (_lib.ptr(v) if k in want else None) for k, v in out.items()}
+    rc = lib.am_lawops_host(s_law, _STRATEGY_CODES[strategy], B, _lib.ptr(e), _lib.ptr(av), _lib.ptr(dav),
+                            ptr["sigma"], ptr["A"], ptr["f"], ptr["dfda"], ptr["dfde"], _lib.ptr(Cv))
+    _lib.check(rc, "LawOps")
+    res = {"sigma": out["sigma"].reshape(batch + (6,)), "A": out["A"][:, :m].reshape(batch + (m,)),
+           "f": out["f"][:, :m].reshape(batch + (m,)), "dfda": out["dfda"][:, :m, :m].reshape(batch + (m, m)),
+           "dfde": out["dfde"][:, :m].reshape(batch + (m, 6))}
+    if C:
+        res["C"] = Cv.reshape(batch + (6, 6))
+    return res
+
+
+class LawOps:
+    """Uniform evaluation surface of a law under a strategy (gsm.py:412-566), on the device.
+
+    Array operations only: the ``*_generic`` methods of the reference run
+    Python payloads through Python potentials, which have no device
+    counterpart.
+    """
+
+    def __init__(self, law, strategy):
+        if strategy not in ("automatic", "semi-automatic"):
+            raise ValueError(f"unsupported strategy {strategy!r}")
+        if strategy == "semi-automatic" and not law.has_hand_partials:
+            raise ValueError("law does not ship hand-coded partials")
+        _lib.make_law(law)  # ConfigError for laws without device potentials
+        self.law = law
+        self.strategy = strategy
+        self.m = law.m
+
+    def stress(self, eps, a):
+        return _lawops(self.law, self.strategy, eps, a, want=("sigma",))["sigma"]
+
+    def gen_stress(self, eps, a):
+        return _lawops(self.law, self.strategy, eps, a, want=("A",))["A"]
+
+    def rhs(self, eps, a):
+        return _lawops(self.law, self.strategy, eps, a, want=("f",))["f"]
+
+    def rhs_and_jacobians(self, eps, a):
+        """RHS with d f/d a and d f/d eps, shape (..., m, m) and (..., m, 6)."""
+        r = _lawops(self.law, self.strategy, eps, a, want=("f", "dfda", "dfde"))
+        return r["f"], r["dfda"], r["dfde"]
+
+    def stress_and_tangent(self, eps, a, da_deps):
+        """Stress and consistent tangent C = d2w/de2 + d2w/dade . da/de."""
+        r = _lawops(self.law, self.strategy, eps, a, da=da_deps, want=("sigma",), C=True)
+        return r["sigma"], r["C"]
+
+    def elastic_tangent(self, eps, a):
+        """Second strain derivative of omega (exact tangent when a is frozen)."""
+        return _lawops(self.law, self.strategy, eps, a, want=(), C=True)["C"]
 
 
 def stress(law, eps, a, strategy="automatic"):
     """Stress sigma = domega/deps at (eps, a)."""
-    return _constitutive(law, eps, a, strategy)[0]
+    return _lawops(law, strategy, eps, a, want=("sigma",))["sigma"]
 
 
 def generalized_stress(law, eps, a, strategy="automatic"):
     """Generalized stresses A = -domega/da at (eps, a)."""
-    return _constitutive(law, eps, a, strategy)[1]
+    return _lawops(law, strategy, eps, a, want=("A",))["A"]
 
 
 def evolution_rhs(law, eps, a, strategy="automatic"):
     """Evolution right-hand side f(eps, a) = dpsi/dA(-domega/da)."""
-    return _constitutive(law, eps, a, strategy)[2]
+    return _lawops(law, strategy, eps, a, want=("f",))["f"]
 
 
 def rhs_jacobian(law, eps, a, strategy="automatic"):
     """Jacobian df/da of the evolution right-hand side."""
-    return _constitutive(law, eps, a, strategy)[3]
+    return _lawops(law, strategy, eps, a, want=("dfda",))["dfda"]
 
 
 def rhs_strain_jacobian(law, eps, a, strategy="automatic"):
     """Jacobian df/deps of the evolution right-hand side."""
-    return _constitutive(law, eps, a, strategy)[4]
+    return _lawops(law, strategy, eps, a, want=("dfde",))["dfde"]
+
+
+def conventional_evaluate(law, eps_n, a_n, eps_np1, h, want_tangent=False):
+    """Material-specific single-step evaluation (radial return, gsm.py:605-609).
+
+    Runs the device radial return (csrc/conventional.cuh); a stalled scalar
+    Newton raises ``NewtonError`` like gsm.py:377-378.
+    """
+    if not law.has_conventional:
+        raise ValueError("law has no conventional evaluation routine")
+    return law.conventional_step(eps_n, a_n, eps_np1, h, want_tangent)
+
+
+def _conventional_step(law, eps_n, a_n, eps_np1, h, want_tangent):
+    """MichelSuquet.conventional_step (gsm.py:332-404) on the device."""
+    from .evaluator import StrategyConfig, _evaluate_arrays_status
+
+    eps_np1 = np.asarray(eps_np1, dtype=float)
+    a_n = np.asarray(a_n, dtype=float)
+    squeeze = eps_np1.ndim == 1
+    if squeeze:
+        eps_np1 = eps_np1[None]
+        a_n = np.broadcast_to(a_n, (1, law.m))
+    batch = eps_np1.shape[:-1]
+    B = int(np.prod(batch, dtype=np.int64))
+    hv = np.broadcast_to(np.asarray(h, dtype=float), batch).reshape(B)
+    a2 = np.broadcast_to(a_n, batch + (law.m,)).reshape(B, law.m)
+    e2 = eps_np1.reshape(B, 6)
+    cfg = StrategyConfig(strategy="conventional", integrator="implicit-euler")
+    r, rc, _ = _evaluate_arrays_status(law, cfg, e2, a2, e2, hv, want_tangent)
+    _lib.check(rc, "conventional_step")
+    sigma = r.sigma.reshape(batch + (6,))
+    a_new = r.a.reshape(batch + (law.m,))
+    C = None if r.C is None else r.C.reshape(batch + (6, 6))
+    if squeeze:
+        sigma, a_new = sigma[0], a_new[0]
+        C = None if C is None else C[0]
+    return sigma, a_new, C

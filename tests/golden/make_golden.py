@@ -319,6 +319,44 @@ def make_constitutive():
     )
 
 
+# ---------------------------------------------------------------- lawops
+def make_lawops():
+    """LawOps under both strategies (gsm.py:412-566) and conventional_evaluate (gsm.py:605-609)."""
+    law = gsm.MichelSuquet()
+    rng = np.random.default_rng(4)
+    B = 128
+    eps = rng.normal(0, 2e-3, (B, 6))
+    a = np.zeros((B, 7))
+    a[:, :6] = rng.normal(0, 5e-4, (B, 6))
+    a[:, 6] = np.abs(rng.normal(0, 1e-3, B))
+    a[:8] = 0.0
+    eps[:4] = 0.0
+    da = rng.normal(0, 1.0, (B, 7, 6))
+    out = {"eps": eps, "a": a, "da": da}
+    for tag, strat in (("auto", "automatic"), ("semi", "semi-automatic")):
+        ops = gsm.LawOps(law, strat)
+        out[tag + "_stress"] = ops.stress(eps, a)
+        out[tag + "_gen_stress"] = np.stack([np.asarray(ops.gen_stress(eps[i], a[i]), dtype=float)
+                                             for i in range(B)])
+        f, J, Je = ops.rhs_and_jacobians(eps, a)
+        out[tag + "_rhs"], out[tag + "_dfda"], out[tag + "_dfde"] = f, J, Je
+        sig, C = ops.stress_and_tangent(eps, a, da)
+        out[tag + "_st_sigma"], out[tag + "_st_C"] = sig, C
+        out[tag + "_elastic_C"] = ops.elastic_tangent(eps, a)
+    le = gsm.LinearElastic(300e9, 0.25)
+    for tag, strat in (("auto", "automatic"), ("semi", "semi-automatic")):
+        ops = gsm.LawOps(le, strat)
+        out["le_" + tag + "_stress"] = ops.stress(eps, np.zeros((B, 0)))
+        out["le_" + tag + "_C"] = ops.stress_and_tangent(eps, np.zeros((B, 0)), np.zeros((B, 0, 6)))[1]
+    # conventional radial return: a loading step from the states above
+    eps_np1 = eps + rng.normal(0, 3e-3, (B, 6))
+    h = np.full(B, 0.05)
+    h[:3] = 0.0
+    sig, a_new, C = gsm.conventional_evaluate(law, eps, a, eps_np1, h, want_tangent=True)
+    out.update(conv_eps_np1=eps_np1, conv_h=h, conv_sigma=sig, conv_a=a_new, conv_C=C)
+    save("lawops.npz", **out)
+
+
 # ---------------------------------------------------------------- fourier
 def make_fourier():
     rng = np.random.default_rng(5)
@@ -467,6 +505,7 @@ if __name__ == "__main__":
         "adaptive": make_adaptive,
         "semi": make_semi,
         "constitutive": make_constitutive,
+        "lawops": make_lawops,
         "fourier": make_fourier,
         "config1": make_config1,
         "path16": make_path16_conv,
