@@ -156,7 +156,7 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def basic_scheme(n, lib, dev, dist=None):
+def basic_scheme(n, lib, dev, dist=None, warm=False):
     """Basic-scheme iterations/s on config 4's microstructure (toy_mmc_grid(n),
     elasto-viscoplastic matrix + elastic fibre), load step 1 of
     LoadingPath(steps=20) with mixed BCs, device-resident; per-phase times
@@ -174,7 +174,7 @@ def basic_scheme(n, lib, dev, dist=None):
     grid = H.toy_mmc_grid(n)
     comm = D.comm_from_torch() if dist is not None else None
     try:
-        hom = H.Homogenizer(grid, cfg, comm=comm)
+        hom = H.Homogenizer(grid, cfg, comm=comm, newton_warm_start=warm)
         ok = 1
     except Exception as exc:  # noqa: BLE001 - reported in the JSON line
         hom, ok, why = None, 0, f"{type(exc).__name__}: {exc}"
@@ -229,7 +229,7 @@ def basic_scheme(n, lib, dev, dist=None):
     }
 
 
-def loading_path_bench(n, dev, dist=None, steps=20):
+def loading_path_bench(n, dev, dist=None, steps=20, warm=False):
     """Config 3: the full 20-step loading path (tension-compression, mixed BC,
     reference update every step) on toy_mmc_grid(n) through the public
     run_loading_path, device time on the solver stream via am_solver_timing
@@ -244,7 +244,7 @@ def loading_path_bench(n, dev, dist=None, steps=20):
     comm = D.comm_from_torch() if dist is not None else None
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    recs = H.run_loading_path(grid, H.LoadingPath(steps=steps), cfg, comm=comm)
+    recs = H.run_loading_path(grid, H.LoadingPath(steps=steps), cfg, comm=comm, newton_warm_start=warm)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     its = int(sum(r["iterations"] for r in recs))
@@ -416,6 +416,28 @@ def main():
             path = loading_path_bench(args.path, dev, dist)
         except Exception as exc:  # noqa: BLE001
             path = {"metric": "basic-scheme iterations/s over the loading path", "error": f"{type(exc).__name__}: {exc}"}
+
+    # the same runs with the solver's Newton warm start (opt-in, not in the
+    # reference: identical basic-scheme iteration counts, fields equal to
+    # round-off, fewer per-voxel Newton iterations)
+    warm_note = ("Homogenizer(newton_warm_start=True): each voxel's Newton starts at its previous basic-scheme "
+                 "iterate instead of a_n (opt-in; same equations and tolerance, identical basic-scheme iterations)")
+    if basic is not None and "error" not in basic:
+        try:
+            bw = basic_scheme(args.basic, lib, dev, dist, warm=True)
+            basic["newton_warm_start"] = {k: bw[k] for k in ("value", "unit", "iterations", "ms_per_iteration",
+                                                             "phase_ms_per_iteration")}
+            basic["newton_warm_start"]["note"] = warm_note
+        except Exception as exc:  # noqa: BLE001
+            basic["newton_warm_start"] = {"error": f"{type(exc).__name__}: {exc}"}
+    if path is not None and "error" not in path:
+        try:
+            pw = loading_path_bench(args.path, dev, dist, warm=True)
+            path["newton_warm_start"] = {k: pw[k] for k in ("value", "unit", "seconds", "iterations_total",
+                                                            "sig_xx_final", "C11_final")}
+            path["newton_warm_start"]["note"] = warm_note
+        except Exception as exc:  # noqa: BLE001
+            path["newton_warm_start"] = {"error": f"{type(exc).__name__}: {exc}"}
 
     if rank != 0:
         if dist is not None:

@@ -220,6 +220,13 @@ int am_solver_set_mean(am_solver *h, const double *ebar_n);
  * The converged fields stay on the device (am_solver_get_field). */
 int am_solver_solve_step(am_solver *h, const double *ebar_target, double dt, const uint8_t *free_mask,
                          double tol, int max_iterations, am_stepinfo *info, double *history, int history_cap);
+/* Newton warm start inside solve_step (implicit Euler only; default off):
+ * from the second basic-scheme iteration of a step on, each voxel's
+ * Newton starts at its previous iterate's state instead of a_n.  Same
+ * equations and tolerance (odeint.py:357-401), fewer iterations; results
+ * agree with the cold start to round-off, not bit for bit.  No reference
+ * counterpart (the reference always starts at a_n, odeint.py:371). */
+int am_solver_set_warm_start(am_solver *h, int on);
 /* Homogenizer.commit_step (homogenize.py:474-480) for the solver's eps */
 int am_solver_commit(am_solver *h, const double *ebar);
 /* Homogenizer.evaluate_field (homogenize.py:389-421) of the device eps,

@@ -21,6 +21,7 @@ struct KArgs {
     const int64_t* gidx;  // optional gather/scatter index for eps_n / eps_np1 / sigma
     const double* eps_n;
     const double* a_n;
+    const double* a_start;  // optional first Newton iterate (same layout as a_n; may alias a_out)
     const double* eps_np1;
     const double* dt;
     double dt_scalar;

@@ -94,7 +94,11 @@ __global__ void __launch_bounds__(128, AM_K1_MINB_N) k_material(Law L, KArgs k) 
         io.eps(en, ep);
         io.load_a<m>(k.a_n, an);
         int it = 0;
-        const int st = newton_point<Law, Mode>(L, k.ncfg, en, an, ep, io.dt(), a, it);
+        // warm start (solver option): the previous basic-scheme iterate
+        double as[ms];
+        const bool warm = !Raw && k.a_start;
+        if (warm) io.load_a<m>(k.a_start, as);
+        const int st = newton_point<Law, Mode>(L, k.ncfg, en, an, ep, io.dt(), a, it, warm ? as : nullptr);
         if constexpr (Raw) {
             io.store_a<m>(a);
         } else {

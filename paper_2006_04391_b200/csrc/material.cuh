@@ -602,10 +602,16 @@ struct NewtonState {
 
     // MaterialStepProblem set-up; false when no iteration is needed
     // (no state, or frozen dt == 0: a = a_n)
-    AM_HD bool init(const Law& L, const double* eps_n, const double* a_n, const double* eps_np1, double dt) {
+    // a_start: optional first iterate (default a_n, odeint.py:371)
+    AM_HD bool init(const Law& L, const double* eps_n, const double* a_n, const double* eps_np1, double dt,
+                    const double* a_start = nullptr) {
         iters = 0;
 #pragma unroll
         for (int i = 0; i < m; ++i) a0[i] = a[i] = a_n[i];
+        if (a_start && m > 0 && dt != 0.0) {
+#pragma unroll
+            for (int i = 0; i < m; ++i) a[i] = a_start[i];
+        }
         if (m == 0 || dt == 0.0) return false;
         h = dt;
         step_strain(eps_n, eps_np1, dt, e1);
@@ -683,10 +689,10 @@ struct NewtonState {
 
 template <class Law, int Mode>
 AM_HD int newton_point(const Law& L, const NewtonCfg& cfg, const double* eps_n, const double* a_n,
-                       const double* eps_np1, double dt, double* a, int& iters) {
+                       const double* eps_np1, double dt, double* a, int& iters, const double* a_start = nullptr) {
     NewtonState<Law, Mode> S;
     int r = 1;
-    if (S.init(L, eps_n, a_n, eps_np1, dt))
+    if (S.init(L, eps_n, a_n, eps_np1, dt, a_start))
         while ((r = S.step(L, cfg)) == 0) {
         }
 #pragma unroll

@@ -484,6 +484,7 @@ struct am_solver {
     double lam = 0.0, mu = 0.0;
     double ebar_n[6] = {0, 0, 0, 0, 0, 0};
     bool pending = false;
+    bool warm_start = false;  // Newton from the previous iterate's state (am_solver_set_warm_start)
     am::DevBasis db = am::DevBasis::make();
     bool timing = false;
     cudaEvent_t ev[6] = {};
@@ -616,7 +617,9 @@ static int inverse(am_solver* h, double2* Slab::*src, double* Slab::*field) {
 }
 
 // K1 over every phase of every local slab
-static int material_sweep(am_solver* h, double dt) {
+// warm: start each voxel's Newton from its pending state (the previous
+// basic-scheme iterate) instead of a_n (am_solver_set_warm_start)
+static int material_sweep(am_solver* h, double dt, bool warm = false) {
     for (auto& s : h->slabs) {
         AM_CUDA(cudaMemsetAsync(s.flags, 0, sizeof(uint32_t), h->stream));
         AM_CUDA(cudaMemsetAsync(s.subs, 0, sizeof(unsigned long long), h->stream));
@@ -627,6 +630,7 @@ static int material_sweep(am_solver* h, double dt) {
             k.B = p.count;
             k.gidx = p.gidx;
             k.eps_n = s.eps_n; k.eps_np1 = s.eps; k.a_n = p.a_n; k.dt = nullptr; k.dt_scalar = dt;
+            k.a_start = (warm && p.m && h->cfg.integrator == AM_INTEGRATOR_IMPLICIT_EULER) ? p.a_pend : nullptr;
             k.le = {s.Nl, 1}; k.la = {p.count, 1}; k.lc = {0, 0};
             k.sigma = s.sigma; k.a_out = p.a_pend; k.C = nullptr;
             k.iters = nullptr; k.status = nullptr; k.flags = s.flags;
@@ -947,7 +951,7 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
     };
     for (int it = 1; it <= max_iterations; ++it) {
         AM_TRY(mark(0));
-        AM_TRY(material_sweep(h, dt));
+        AM_TRY(material_sweep(h, dt, h->warm_start && it > 1));
         AM_TRY(mark(1));
         AM_TRY(forward(h, &Slab::sigma, &Slab::S));
         AM_TRY(mark(2));
@@ -1020,6 +1024,12 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
     }
     return fail(AM_ERR_NOT_CONVERGED, "basic scheme did not converge in %d iterations (last residual %.3e)",
                 max_iterations, info->residual);
+}
+
+extern "C" int am_solver_set_warm_start(am_solver* h, int on) {
+    if (!h) return fail(AM_ERR_ARG, "null solver");
+    h->warm_start = on != 0;
+    return AM_OK;
 }
 
 // eps_n <- eps, ebar_n <- ebar, a_n <- pending (homogenize.py:474-480)

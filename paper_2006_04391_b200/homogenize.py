@@ -262,8 +262,13 @@ class Homogenizer:
     copies.
     """
 
-    def __init__(self, grid, cfg, threads=1, tol=1e-5, max_iterations=5000, slabs=1, comm=None):
-        """``slabs`` > 1 runs the multi-GPU slab algorithm from this process on
+    def __init__(self, grid, cfg, threads=1, tol=1e-5, max_iterations=5000, slabs=1, comm=None,
+                 newton_warm_start=False):
+        """``newton_warm_start`` (implicit Euler; not in the reference) starts
+        each voxel's Newton at its previous basic-scheme iterate instead of
+        a_n from the second iteration of a step on: same equations and
+        tolerance, fewer Newton iterations, results equal to round-off.
+        ``slabs`` > 1 runs the multi-GPU slab algorithm from this process on
         one device (x-slabs, all-to-all transposes as device copies); ``comm``
         (distributed.Comm) makes this process one rank of an NCCL-connected
         slab decomposition, in which case host fields are the rank's x-slab
@@ -295,6 +300,8 @@ class Homogenizer:
             self._local_dims = tuple(grid.dims)
         _lib.check(rc, "Homogenizer")
         self._h = h
+        if newton_warm_start:
+            _lib.check(self._lib.am_solver_set_warm_start(h, 1), "newton_warm_start")
         if comm is not None and comm.allgather is not None and comm.transport == "p2p":
             # fused transposes over NVLink: swap the spectrum buffers' IPC handles
             mine = ctypes.create_string_buffer(128)
@@ -464,14 +471,16 @@ class Homogenizer:
 
 
 def run_loading_path(grid, path, cfg, update_reference=True, threads=1, tol=1e-5, max_iterations=5000, slabs=1,
-                     comm=None):
+                     comm=None, newton_warm_start=False):
     """March the loading path; one record dict per step (homogenize.py:485-528).
 
     Device-resident: per step the basic scheme, then (update_reference) the
     tangent sweep fused with reference_update, commit, new reference.
-    ``slabs`` / ``comm``: see Homogenizer (every rank returns the same records).
+    ``slabs`` / ``comm`` / ``newton_warm_start``: see Homogenizer (every rank
+    returns the same records).
     """
-    hom = Homogenizer(grid, cfg, threads=threads, tol=tol, max_iterations=max_iterations, slabs=slabs, comm=comm)
+    hom = Homogenizer(grid, cfg, threads=threads, tol=tol, max_iterations=max_iterations, slabs=slabs, comm=comm,
+                      newton_warm_start=newton_warm_start)
     lib = hom._lib
     times = path.times()
     eps_targets = path.eps_xx(times)

@@ -131,12 +131,14 @@ def test_path8_manual_loop(H, AUTO):
     assert rel(grid.state[0], g["state0"]) < TOL
 
 
-def test_run_loading_path_16(H, AUTO):
-    """Full 20-step path at 16^3: identical iteration counts."""
+@pytest.mark.parametrize("warm", [False, True])
+def test_run_loading_path_16(H, AUTO, warm):
+    """Full 20-step path at 16^3: identical iteration counts
+    (also with the Newton warm start, which changes per-voxel Newton counts only)."""
     g = golden("path16_conv.npz")
     grid = H.toy_mmc_grid(16)
     assert np.array_equal(grid.material_ids, g["ids"])
-    recs = H.run_loading_path(grid, H.LoadingPath(steps=20), AUTO)
+    recs = H.run_loading_path(grid, H.LoadingPath(steps=20), AUTO, newton_warm_start=warm)
     assert [r["iterations"] for r in recs] == g["iterations"].tolist()
     sig = np.stack([r["sig"] for r in recs])
     assert rel(sig[:, 0], g["sig"][:, 0]) < 1e-9
@@ -144,6 +146,28 @@ def test_run_loading_path_16(H, AUTO):
     assert rel([r["C12"] for r in recs], g["C12"]) < 1e-8
     assert rel([r["eps_xx"] for r in recs], g["eps_xx"]) < 1e-9
     assert all(r["mean_substeps"] == 1.0 for r in recs)
+
+
+def test_warm_start_matches_cold(H, AUTO):
+    """Newton warm start: same basic-scheme iterations, fields equal to round-off (32^3, 3 steps)."""
+    out = []
+    for warm in (False, True):
+        hom = H.Homogenizer(H.toy_mmc_grid(32), AUTO, newton_warm_start=warm)
+        path = H.LoadingPath(steps=20)
+        t = path.times()
+        res = []
+        for k in range(1, 4):
+            eb = np.zeros(6)
+            eb[0] = path.eps_xx(t[k])
+            eps, sigma, info = hom.solve_step(eb, t[k] - t[k - 1], free_mask=np.array([False] + [True] * 5))
+            res.append((info.iterations, eps, sigma))
+            hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+        out.append((res, hom.grid.state[0]))
+    (cold, s_cold), (warm, s_warm) = out
+    for (ic, ec, sc), (iw, ew, sw) in zip(cold, warm):
+        assert ic == iw
+        assert rel(ew, ec) < 1e-12 and rel(sw, sc) < 1e-12
+    assert rel(s_warm, s_cold) < 1e-12
 
 
 def test_odd_grid_vs_oracle(H, AUTO):
