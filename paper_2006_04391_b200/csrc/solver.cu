@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -42,6 +43,7 @@
 #include "k1.cuh"
 #include "laws.cuh"
 #include "refupdate.cuh"
+#include "xfused.cuh"
 
 namespace am {
 
@@ -185,6 +187,20 @@ __global__ void k_origin(double2* S, double2* ehat, int64_t cs, Vec6 ebar, doubl
         ehat[c * cs] = make_double2(ebar.v[c] * N, 0.0);
         S[c * cs] = make_double2(ebar.v[c], 0.0);
     }
+}
+
+// origin of the fused update (xfused.cuh) once the host has the new mean
+// strain: ehat(0) = N ebar, and the inverse x transform of the origin bin,
+// ebar along the (ky, kz) = 0 line of the 2-D spectra
+__global__ void k_origin_x(double2* __restrict__ S, double2* __restrict__ ehat, int64_t cs, int64_t xs, int nx,
+                           Vec6 ebar, double N) {
+    const int c = blockIdx.x;
+    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
+        double2 v = S[c * cs + x * xs];
+        v.x += ebar.v[c];
+        S[c * cs + x * xs] = v;
+    }
+    if (threadIdx.x == 0) ehat[c * cs] = make_double2(ebar.v[c] * N, 0.0);
 }
 
 // forward transpose, pack: 2-D spectra P (6, nxl, ny, nzh) -> send blocks
@@ -465,6 +481,8 @@ struct am_solver {
     am_cfg cfg{};
     int nslabs = 1;      // global slab count
     bool multi = false;  // slab (transpose) algorithm vs 3-D cuFFT
+    bool xfused = false; // single slab, nx = 256, AM_XFUSED=1: 2-D cuFFT + fused x transforms (xfused.cuh)
+    int64_t redP = 0;    // offset of the slots after the residual partials in red
     ncclComm_t comm = nullptr;  // nccl mode: this process holds one slab
     std::vector<am::Slab> slabs;  // slabs held by this process
     cufftHandle r3 = 0, c3 = 0;   // 3-D D2Z / Z2D (single slab)
@@ -660,6 +678,27 @@ static int fourier_pass(am_solver* h, bool update, std::vector<double>& out) {
     return reduce_to_host(h, out.data());
 }
 
+// the fused spectral step (xfused.cuh): 2-D spectra of sigma in S ->
+// residual partials per tile + slots, ehat updated, S = 2-D spectra of the
+// next eps without its origin (k_origin_x)
+static int fourier_pass_x(am_solver* h, std::vector<double>& out) {
+    const RefMat ref = RefMat::make(h->lam, h->mu);
+    const int64_t L = h->redlen;
+    Slab& s = h->slabs[0];
+    AM_CUDA(cudaMemsetAsync(h->red, 0, sizeof(double) * L, h->stream));
+    k_finish<<<1, 32, 0, h->stream>>>(s.S, s.sp.cs, 0, s.flags, s.subs, h->red, h->redP);
+    AM_CUDA(cudaGetLastError());
+    const int64_t ncol = (int64_t)h->ny * h->nzh;
+    const int64_t tiles = (ncol + kXJ - 1) / kXJ;
+    int sms = 148;
+    AM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    k_xfourier<<<(unsigned)(kXNB == 2 ? std::min<int64_t>(tiles, sms) : tiles), kXThreads, kXSmem, h->stream>>>(h->nx, h->ny, h->nz, s.sp.cs, ref, s.S, s.ehat, h->red,
+                                                         h->redP);
+    AM_CUDA(cudaGetLastError());
+    out.resize(L);
+    return reduce_to_host(h, out.data());
+}
+
 }  // namespace am
 
 using namespace am;
@@ -742,7 +781,15 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
             }
         }
     }
-    h->redlen = (int64_t)ny * kParts + 10;
+    // fused x transforms on one GPU when nx = 256, opt-in (AM_XFUSED=1):
+    // correct, but slower than cuFFT's x passes + k_fourier at 256^3 so far
+    // (profiles/r01/k1_variants.log, r26)
+    {
+        const char* on = getenv("AM_XFUSED");
+        h->xfused = !h->multi && nx == kXN && on && on[0] == '1';
+    }
+    h->redP = h->xfused ? ((int64_t)ny * h->nzh + kXJ - 1) / kXJ : (int64_t)ny * kParts;
+    h->redlen = h->redP + 10;
     for (int64_t i = 0; i < N; ++i)
         if (law_m(&laws[ids[i]])) ++h->nstate;
     AMC(cudaMalloc(&h->red, sizeof(double) * h->redlen * h->slabs.size()));
@@ -767,6 +814,15 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
         long long n3[3] = {nx, ny, nz};
         ok = plan(&h->r3, 3, n3, nullptr, 1, N, nullptr, 1, (long long)nx * ny * h->nzh, CUFFT_D2Z, 6) &&
              plan(&h->c3, 3, n3, nullptr, 1, (long long)nx * ny * h->nzh, nullptr, 1, N, CUFFT_Z2D, 6);
+        if (ok && h->xfused) {
+            long long n2[2] = {ny, nz};
+            ok = plan(&h->r2, 2, n2, nullptr, 1, (long long)ny * nz, nullptr, 1, (long long)ny * h->nzh, CUFFT_D2Z,
+                      6LL * nx) &&
+                 plan(&h->c2, 2, n2, nullptr, 1, (long long)ny * h->nzh, nullptr, 1, (long long)ny * nz, CUFFT_Z2D,
+                      6LL * nx) &&
+                 cudaFuncSetAttribute(k_xfourier, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXSmem) ==
+                     cudaSuccess;
+        }
     } else {
         long long n2[2] = {ny, nz};
         long long n1[1] = {nx};
@@ -937,7 +993,7 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
     info->residual = 0.0;
     info->mean_substeps = 1.0;  // implicit Euler: one substep per voxel (evaluator.py:130)
     const double Nd = (double)h->N;
-    const int64_t P = (int64_t)h->ny * kParts;
+    const int64_t P = h->redP;
     std::vector<double> o;
     auto mark = [&](int i) -> int {
         if (h->timing) AM_CUDA(cudaEventRecord(h->ev[i], h->stream));
@@ -953,9 +1009,15 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
         AM_TRY(mark(0));
         AM_TRY(material_sweep(h, dt, h->warm_start && it > 1));
         AM_TRY(mark(1));
-        AM_TRY(forward(h, &Slab::sigma, &Slab::S));
-        AM_TRY(mark(2));
-        AM_TRY(fourier_pass(h, true, o));  // synchronises the stream
+        if (h->xfused) {
+            AM_CUFFT(cufftExecD2Z(h->r2, h->slabs[0].sigma, h->slabs[0].S));
+            AM_TRY(mark(2));
+            AM_TRY(fourier_pass_x(h, o));  // synchronises the stream
+        } else {
+            AM_TRY(forward(h, &Slab::sigma, &Slab::S));
+            AM_TRY(mark(2));
+            AM_TRY(fourier_pass(h, true, o));  // synchronises the stream
+        }
         if (h->timing) {
             AM_CUDA(cudaEventRecord(h->ev[3], h->stream));
             AM_CUDA(cudaEventSynchronize(h->ev[3]));
@@ -1010,12 +1072,19 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
         AM_TRY(mark(4));
         Vec6 eb;
         for (int i = 0; i < 6; ++i) eb.v[i] = ebar[i];
-        for (auto& s : h->slabs)
-            if (s.y0 == 0) {
-                k_origin<<<1, 32, 0, h->stream>>>(s.S, s.ehat, s.sp.cs, eb, Nd);
-                AM_CUDA(cudaGetLastError());
-            }
-        AM_TRY(inverse(h, &Slab::S, &Slab::eps));
+        if (h->xfused) {
+            Slab& s = h->slabs[0];
+            k_origin_x<<<6, 256, 0, h->stream>>>(s.S, s.ehat, s.sp.cs, (int64_t)h->ny * h->nzh, h->nx, eb, Nd);
+            AM_CUDA(cudaGetLastError());
+            AM_CUFFT(cufftExecZ2D(h->c2, s.S, s.eps));
+        } else {
+            for (auto& s : h->slabs)
+                if (s.y0 == 0) {
+                    k_origin<<<1, 32, 0, h->stream>>>(s.S, s.ehat, s.sp.cs, eb, Nd);
+                    AM_CUDA(cudaGetLastError());
+                }
+            AM_TRY(inverse(h, &Slab::S, &Slab::eps));
+        }
         if (h->timing) {
             AM_TRY(mark(5));
             AM_CUDA(cudaEventSynchronize(h->ev[5]));

@@ -1,6 +1,6 @@
 """A few basic-scheme iterations at n^3 for ncu (launch list / full capture).
 
-usage: python tools/basic_profile.py [n] [iterations]
+usage: python tools/basic_profile.py [n] [iterations] [warm]
 """
 import os
 import sys
@@ -13,8 +13,9 @@ from paper_2006_04391_b200.evaluator import StrategyConfig  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 its = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+warm = len(sys.argv) > 3 and sys.argv[3] == "warm"
 hom = H.Homogenizer(H.toy_mmc_grid(n), StrategyConfig(strategy="automatic", integrator="implicit-euler"),
-                    max_iterations=its)
+                    max_iterations=its, newton_warm_start=warm)
 path = H.LoadingPath(steps=20)
 t = path.times()
 eb = np.zeros(6)
