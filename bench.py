@@ -401,6 +401,29 @@ def main():
     if dist is not None:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = world * B / float(e2e_t.item())
+    # the PCIe ceiling of that path: the same bytes as plain concurrent
+    # pinned copies (H2D on one stream, D2H on another), no kernels
+    h2d_b = B * (6 + 7 + 6 + 1) * 8
+    d2h_b = B * (6 + 7 + 36) * 8 + B * 4
+    hin = torch.empty(h2d_b // 8, dtype=torch.float64, pin_memory=True)
+    hout = torch.empty(d2h_b // 8, dtype=torch.float64, pin_memory=True)
+    din, dout = torch.empty_like(hin, device=dev), torch.empty_like(hout, device=dev)
+    s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+    def copies():
+        with torch.cuda.stream(s_in):
+            din.copy_(hin, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            hout.copy_(dout, non_blocking=True)
+
+    copies()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        copies()
+    torch.cuda.synchronize()
+    pcie_ceiling = B / ((time.perf_counter() - t0) / 3)
+    del hin, hout, din, dout
     assert np.array_equal(h_it, iters), "e2e path disagrees with the device path"
     h2d = B * (6 + 7 + 6 + 1) * 8
     d2h = B * (6 + 7 + 36) * 8 + B * 4
@@ -461,7 +484,9 @@ def main():
                      "work_per_launch": f"{fl:.4g} algorithmic fp64 flops per step (SURVEY §8d: 1072*N_it + 2273 per eval); "
                                     "one step = the Newton kernel + the tangent kernel"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "am_eval_batch_host (C ABI), pinned host AoS buffers, 3-stream chunked (2^17 points) H2D|kernels|D2H"},
+                "pcie_ceiling": pcie_ceiling, "frac_of_pcie_ceiling": e2e_value / world / pcie_ceiling,
+                "pcie_ceiling_note": "same bytes as concurrent pinned H2D + D2H copies without kernels (per GPU)",
+                "path": "am_eval_batch_host (C ABI), pinned host AoS buffers, 3-stream chunked (ramp 2^12 .. 2^17 points) H2D|kernels|D2H"},
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
     }

@@ -301,11 +301,18 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
     AM_TRY(P.ensure(chunk));
     AM_CUDA(cudaMemsetAsync(P.flags, 0, sizeof(uint32_t) * HostPipe::kSlots, P.stream[0]));
     AM_CUDA(cudaStreamSynchronize(P.stream[0]));
-    const int64_t nchunks = (B + chunk - 1) / chunk;
-    for (int64_t c = 0; c < nchunks; ++c) {
+    // chunk sizes ramp up from 2^AM_HOST_RAMP_LOG2 so the first D2H starts
+    // early (pipeline fill), then stay at `chunk`
+#ifndef AM_HOST_RAMP_LOG2
+#define AM_HOST_RAMP_LOG2 12
+#endif
+    int64_t lo = 0;
+    for (int64_t c = 0; lo < B; ++c) {
         const int s = int(c % HostPipe::kSlots);
         cudaStream_t st = P.stream[s];
-        const int64_t lo = c * chunk, n = (B - lo) < chunk ? (B - lo) : chunk;
+        int64_t want = chunk;
+        if (AM_HOST_RAMP_LOG2 + c < AM_HOST_CHUNK_LOG2) want = int64_t(1) << (AM_HOST_RAMP_LOG2 + c);
+        const int64_t n = (B - lo) < want ? (B - lo) : want;
         double* d_en = P.in[s];
         double* d_an = d_en + 6 * n;
         double* d_e1 = d_an + 7 * n;
@@ -334,6 +341,7 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
         if (rejected)
             AM_CUDA(cudaMemcpyAsync(rejected + lo, P.iters[s] + n, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
         if (status) AM_CUDA(cudaMemcpyAsync(status + lo, P.status[s], n, cudaMemcpyDeviceToHost, st));
+        lo += n;
     }
     uint32_t flags[HostPipe::kSlots];
     AM_CUDA(cudaMemcpyAsync(flags, P.flags, sizeof(flags), cudaMemcpyDeviceToHost, P.stream[0]));

@@ -148,11 +148,12 @@ def test_run_loading_path_16(H, AUTO, warm):
     assert all(r["mean_substeps"] == 1.0 for r in recs)
 
 
-def test_warm_start_matches_cold(H, AUTO):
+@pytest.mark.parametrize("slabs", [1, 2])
+def test_warm_start_matches_cold(H, AUTO, slabs):
     """Newton warm start: same basic-scheme iterations, fields equal to round-off (32^3, 3 steps)."""
     out = []
     for warm in (False, True):
-        hom = H.Homogenizer(H.toy_mmc_grid(32), AUTO, newton_warm_start=warm)
+        hom = H.Homogenizer(H.toy_mmc_grid(32), AUTO, newton_warm_start=warm, slabs=slabs)
         path = H.LoadingPath(steps=20)
         t = path.times()
         res = []

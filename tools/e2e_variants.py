@@ -37,6 +37,36 @@ if len(sys.argv) > 1 and sys.argv[1] == "--one":
         step()
     ms = (time.perf_counter() - t0) / 5 * 1e3
     print(os.path.basename(os.path.dirname(sys.argv[2])), f"{ms:.3f} ms, {B / ms / 1e3:.3e} evals/s", flush=True)
+elif len(sys.argv) > 1 and sys.argv[1] == "--bw":
+    # raw pinned-host <-> device copy bandwidth: the ceiling of the e2e path
+    import torch
+
+    B = 1 << 20
+    hin = torch.empty(B * 20, dtype=torch.float64, pin_memory=True)
+    hout = torch.empty(B * 50, dtype=torch.float64, pin_memory=True)
+    din = torch.empty_like(hin, device="cuda")
+    dout = torch.empty_like(hout, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for name, fn in (("h2d 168 MB", lambda: din.copy_(hin, non_blocking=True)),
+                     ("d2h 419 MB", lambda: hout.copy_(dout, non_blocking=True))):
+        fn(); torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / 5
+        nb = (hin if name.startswith("h2d") else hout).numel() * 8
+        print(name, f"{nb / dt / 1e9:.1f} GB/s", flush=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        with torch.cuda.stream(s1):
+            din.copy_(hin, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hout.copy_(dout, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 5
+    print(f"concurrent h2d+d2h: {dt * 1e3:.2f} ms per (168 + 419) MB -> e2e ceiling {B / dt:.3e} evals/s", flush=True)
 else:
     libs = [os.path.join(ROOT, "paper_2006_04391_b200", "libautomat.so")]
     libs += sorted(glob.glob(os.path.join(ROOT, "tools", "variants", "*", "libautomat.so")))
