@@ -84,3 +84,26 @@ def test_reference_material_matrix():
     from paper_2006_04391_b200 import homogenize as H
 
     np.testing.assert_array_equal(H.ReferenceMaterial(3.0, 2.0).matrix(), OH.iso_matrix(3.0, 2.0))
+
+
+def test_lawops_strategy_validation():
+    """LawOps / module functions reject strategies like gsm.py:420-427 before touching the device."""
+    from paper_2006_04391_b200 import gsm
+
+    law = gsm.MichelSuquet()
+    with pytest.raises(ValueError):
+        gsm.LawOps(law, "numeric")
+    with pytest.raises(ValueError):
+        gsm.LawOps(law, "conventional")  # the class takes automatic / semi-automatic only
+
+    class NoHand(gsm.GsmDefinition):
+        m = 0
+
+    with pytest.raises(ValueError):
+        gsm.LawOps(NoHand(), "semi-automatic")
+    with pytest.raises(ValueError):
+        gsm.stress(NoHand(), np.zeros(6), np.zeros(0), strategy="conventional")  # conventional -> semi
+    with pytest.raises(ValueError):
+        gsm.evolution_rhs(law, np.zeros(6), np.zeros(7), strategy="numeric")
+    with pytest.raises(ValueError):
+        gsm.conventional_evaluate(gsm.LinearElastic(1e9, 0.3), np.zeros(6), np.zeros(0), np.zeros(6), 0.1)

@@ -1,6 +1,6 @@
 """Config 5 on one GPU: 512^3 high-contrast composite (fibre E = 3000 GPa,
 SURVEY.md §8d), load step 1 of LoadingPath(steps=20), device memory and
-basic-scheme iterations/s.  usage: python tools/config5_probe.py [n]"""
+basic-scheme iterations/s.  usage: python tools/config5_probe.py [n] [warm]"""
 import json
 import os
 import sys
@@ -15,11 +15,12 @@ from paper_2006_04391_b200 import _lib, gsm, homogenize as H  # noqa: E402
 from paper_2006_04391_b200.evaluator import StrategyConfig  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+warm = len(sys.argv) > 2 and sys.argv[2] == "warm"
 t0 = time.perf_counter()
 grid = H.toy_mmc_grid(n, fiber_law=gsm.LinearElastic(3000e9, 0.25))
 t_geo = time.perf_counter() - t0
 free0, total = torch.cuda.mem_get_info()
-hom = H.Homogenizer(grid, StrategyConfig(strategy="automatic", integrator="implicit-euler"))
+hom = H.Homogenizer(grid, StrategyConfig(strategy="automatic", integrator="implicit-euler"), newton_warm_start=warm)
 free1, _ = torch.cuda.mem_get_info()
 lib = _lib.load()
 _lib.check(lib.am_solver_timing(hom._h, 1, None))
@@ -36,7 +37,7 @@ ph = np.zeros(5)
 _lib.check(lib.am_solver_timing(hom._h, -1, _lib.ptr(ph)))
 k = ph[4]
 print(json.dumps({
-    "grid": n, "voxels": n ** 3, "fibre": "LinearElastic(3000e9, 0.25)", "geometry_s": round(t_geo, 2),
+    "grid": n, "voxels": n ** 3, "newton_warm_start": warm, "fibre": "LinearElastic(3000e9, 0.25)", "geometry_s": round(t_geo, 2),
     "device_bytes_solver": int(free0 - free1), "device_total": int(total),
     "iterations": info.iterations, "seconds": wall, "it_per_s": info.iterations / wall,
     "phase_ms_per_iteration": {"material": ph[0] / k, "d2z": ph[1] / k, "fourier": ph[2] / k,
