@@ -377,6 +377,41 @@ def main():
     peak = ctypes.c_double(0.0)
     _lib.check(lib.am_probe_fp64_tflops(5, ctypes.byref(peak)))
 
+    # ---- the paper's strategy comparison on the same batch (stress + tangent,
+    # device-resident): every strategy x integrator route the reference offers
+    strategies = {}
+    for strat, integ in (("automatic", "implicit-euler"), ("semi-automatic", "implicit-euler"),
+                         ("conventional", "implicit-euler"), ("automatic", "ode12"), ("automatic", "ode23"),
+                         ("semi-automatic", "ode23"), ("semi-automatic", "ode23s")):
+        c2 = _lib.make_cfg(StrategyConfig(strategy=strat, integrator=integ))
+
+        def run(c2=c2):
+            rc = lib.am_eval_batch(s_law, c2, B, d_en.data_ptr(), d_an.data_ptr(), d_ep.data_ptr(), d_dt.data_ptr(),
+                                   0.0, 1, d_sig.data_ptr(), d_a.data_ptr(), d_C.data_ptr(), d_it.data_ptr(), None,
+                                   d_st.data_ptr(), d_fl.data_ptr(), sp)
+            if rc:
+                _lib.check(rc)
+
+        try:
+            run()
+            run()
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for _ in range(5):
+                run()
+            f1.record(stream)
+            torch.cuda.synchronize()
+            t_ms = f0.elapsed_time(f1) / 5
+            strategies[f"{strat}/{integ}"] = {
+                "evals_per_s": B / (t_ms * 1e-3), "ms": t_ms,
+                ("mean_newton_iters" if integ == "implicit-euler" else "mean_substeps"):
+                    float(d_it.double().mean().item())}
+        except Exception as exc:  # noqa: BLE001
+            strategies[f"{strat}/{integ}"] = {"error": f"{type(exc).__name__}: {exc}"}
+    step()  # leave the headline route's outputs in the buffers
+    torch.cuda.synchronize()
+
     # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
     pin = lambda shape, dtype=torch.float64: torch.empty(shape, dtype=dtype, pin_memory=True).numpy()  # noqa: E731
     h_en, h_an, h_ep, h_dt = pin((B, 6)), pin((B, 7)), pin((B, 6)), pin((B,))
@@ -490,6 +525,9 @@ def main():
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
     }
+    line["strategies"] = strategies
+    line["strategies_note"] = ("config-2 batch, stress + tangent, device-resident, 5 launches each after 2 warm-up; "
+                               "conventional = the paper's hand-derived radial return baseline")
     if path is not None:
         line["loading_path"] = path
     if basic is not None:

@@ -124,21 +124,49 @@ struct SemiLaw<MichelSuquetLaw> {
 
     // rhs_jac_generic (gsm.py:463-481) on plain values: f, d f/d a (dense
     // leading 6 columns; column 6 is the empty sum 0), d f/d eps
-    AM_HD void rhs_jac(const double* e, const double* a, double* f, double (*J)[6], double (*Je)[6]) const {
+    template <bool WithJe>
+    AM_HD void rhs_jac_t(const double* e, const double* a, double* f, double (*J)[6], double (*Je)[6]) const {
         double psi2[7][7];
         auto Av = hand_gen_stress(tup(plain(e[0]), plain(e[1]), plain(e[2]), plain(e[3]), plain(e[4]), plain(e[5])),
                                   tup(plain(a[0]), plain(a[1]), plain(a[2]), plain(a[3]), plain(a[4]), plain(a[5]),
                                       plain(a[6])));
-        flow_pieces(Av, [&](const auto& gdot_, const auto& Pt, const auto& x, const auto& denom_, double gate) {
-            const double gdot = gdot_.v, denom = denom_.v;
+        flow_pieces(Av, [&](const auto&, const auto& Pt, const auto& x, const auto& denom_, double gate) {
+            const double denom = denom_.v;
             const double P[6] = {get<0>(Pt).v, get<1>(Pt).v, get<2>(Pt).v, get<3>(Pt).v, get<4>(Pt).v, get<5>(Pt).v};
-            const double gprime = (base.eps0_dot * base.n / base.sigma_d) * ::pow(x.v, base.n - 1.0);
+            // x^n (gdot) and x^(n-1) (gprime) from one power, as the
+            // automatic path's powjet (ad.cuh): <= 1e-14 relative to pow()
+            const double xv = x.v, c = base.n;
+            double p1, pn;
+            if (xv > 0.0) {
+#ifdef AM_EXACT_POW
+                p1 = ::pow(xv, c - 1.0);
+                pn = ::pow(xv, c);
+#else
+                p1 = ::exp((c - 1.0) * ::log(xv));
+                pn = p1 * xv;
+#endif
+            } else {
+                p1 = ::pow(xv, c - 1.0);
+                pn = ::pow(xv, c);
+            }
+            const double gdot = base.eps0_dot * pn;
+            const double gprime = (base.eps0_dot * base.n / base.sigma_d) * p1;
+            // x / denom for the 36 entries: the correctly rounded reciprocal
+            // and one FMA correction of x * rd give the correctly rounded
+            // quotient (Markstein), i.e. the bits of the IEEE division
+            const double rd = 1.0 / denom;
+            auto qdiv = [&](double num) {
+                const double q = num * rd;
+                return fma(fma(-q, denom, num), rd, q);
+            };
+#pragma unroll
             for (int i = 0; i < 6; ++i) {
                 f[i] = gdot * P[i];
                 const double dup_i = i < 3 ? 1.5 : 3.0;
+#pragma unroll
                 for (int j = 0; j < 6; ++j) {
                     const double dev = (i == j ? 1.0 : 0.0) - ((i < 3 && j < 3) ? 1.0 / 3.0 : 0.0);
-                    const double curv = (dup_i * dev - P[i] * P[j]) / denom * gate;
+                    const double curv = qdiv(dup_i * dev - P[i] * P[j]) * gate;
                     psi2[i][j] = gprime * P[i] * P[j] + gdot * curv;
                 }
                 psi2[i][6] = gprime * P[i];
@@ -148,30 +176,44 @@ struct SemiLaw<MichelSuquetLaw> {
             f[6] = gdot;
             return 0;
         });
-        // d2w_aa = [Ce + (2/3) Hmat, 0; 0, 0], d2w_ae = [-Ce; 0] (gsm.py:221-227)
+        // d2w_aa = [Ce + (2/3) Hmat, 0; 0, 0], d2w_ae = [-Ce; 0] (gsm.py:221-227).
+        // The reference sums psi2[i][j] * w[j][k] over the j with w[j][k] != 0
+        // in increasing j: for a normal column k < 3 that is j = 0, 1, 2 (the
+        // off-diagonal entries are lam, skipped when lam == 0), for a shear
+        // column only j = k.  The sparsity is spelled out at compile time.
         const double lam = base.lam, mu = base.mu, H = base.H;
         const double k23 = 2.0 / 3.0;
-        double waa[6][6], wae[6][6];
-        for (int i = 0; i < 6; ++i)
-            for (int j = 0; j < 6; ++j) {
-                double ce = 0.0;
-                if (i < 3 && j < 3) ce = (i == j) ? lam + 2.0 * mu : lam;
-                else if (i == j) ce = mu;
-                const double hm = (i == j) ? k23 * (i < 3 ? H : H / 2.0) : 0.0;
-                waa[i][j] = ce + hm;
-                wae[i][j] = -ce;
-            }
+        const bool lam_nz = lam != 0.0;
+        const double aa_n = lam + 2.0 * mu + k23 * H, aa_s = mu + k23 * (H / 2.0);
+        const double ae_n = -(lam + 2.0 * mu), ae_o = -lam, ae_s = -mu;
+#pragma unroll
         for (int i = 0; i < 7; ++i) {
-            for (int k = 0; k < 6; ++k) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
                 double s = 0.0, se = 0.0;
-                for (int j = 0; j < 6; ++j) {  // skip structural zeros like the reference
-                    if (waa[j][k] != 0.0) s += psi2[i][j] * waa[j][k];
-                    if (wae[j][k] != 0.0) se += psi2[i][j] * wae[j][k];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    if (j == k) {
+                        s += psi2[i][j] * aa_n;
+                        se += psi2[i][j] * ae_n;
+                    } else if (lam_nz) {
+                        s += psi2[i][j] * lam;
+                        se += psi2[i][j] * ae_o;
+                    }
                 }
                 J[i][k] = -s;
-                if (Je) Je[i][k] = -se;
+                if (WithJe) Je[i][k] = -se;
+            }
+#pragma unroll
+            for (int k = 3; k < 6; ++k) {
+                J[i][k] = -(0.0 + psi2[i][k] * aa_s);
+                if (WithJe) Je[i][k] = -(0.0 + psi2[i][k] * ae_s);
             }
         }
+    }
+    AM_HD void rhs_jac(const double* e, const double* a, double* f, double (*J)[6], double (*Je)[6]) const {
+        if (Je) rhs_jac_t<true>(e, a, f, J, Je);
+        else rhs_jac_t<false>(e, a, f, J, nullptr);
     }
 
     AM_HD void Ce(double (*C)[6]) const {
