@@ -1,4 +1,6 @@
-"""One semi-automatic implicit-Euler evaluation of 2^18 config-2 points (stress + tangent) for ncu."""
+"""Two evaluations of 2^18 config-2 points (stress + tangent) for ncu.
+
+usage: python tools/semi_profile.py [strategy] [integrator]"""
 import os
 import sys
 
@@ -9,6 +11,7 @@ from paper_2006_04391_b200.workloads import config2_batch  # noqa: E402
 
 strategy = sys.argv[1] if len(sys.argv) > 1 else "semi-automatic"
 en, an, ep, dt = config2_batch(1 << 18)
-cfg = StrategyConfig(strategy=strategy, integrator="implicit-euler")
+integrator = sys.argv[2] if len(sys.argv) > 2 else "implicit-euler"
+cfg = StrategyConfig(strategy=strategy, integrator=integrator)
 for _ in range(2):
     evaluate_arrays(gsm.MichelSuquet(), cfg, en, an, ep, dt, want_tangent=True)
