@@ -1,6 +1,6 @@
 """Per-phase basic-scheme timing (load step 1, toy_mmc_grid(n)) for libautomat variants.
 
-usage (GPU box): python tools/basic_variants.py [n] [max_iterations]
+usage (GPU box): python tools/basic_variants.py [n] [max_iterations] [cold|warm]
 Also prints the Newton-iteration histogram of the converged sweep.
 """
 import glob
@@ -12,6 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if len(sys.argv) > 1 and sys.argv[1] == "--one":
     os.environ["AM_LIB"] = sys.argv[2]
     n, its = int(sys.argv[3]), int(sys.argv[4])
+    warm = len(sys.argv) > 5 and sys.argv[5] == "warm"
     sys.path.insert(0, ROOT)
     import numpy as np
 
@@ -20,7 +21,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--one":
 
     cfg = StrategyConfig(strategy="automatic", integrator="implicit-euler")
     grid = H.toy_mmc_grid(n)
-    hom = H.Homogenizer(grid, cfg, max_iterations=its)
+    hom = H.Homogenizer(grid, cfg, max_iterations=its, newton_warm_start=warm)
     lib = _lib.load()
     _lib.check(lib.am_solver_timing(hom._h, 1, None))
     path = H.LoadingPath(steps=20)
@@ -48,7 +49,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "--one":
 else:
     n = sys.argv[1] if len(sys.argv) > 1 else "256"
     its = sys.argv[2] if len(sys.argv) > 2 else "5000"
+    mode = sys.argv[3] if len(sys.argv) > 3 else "cold"
     libs = [os.path.join(ROOT, "paper_2006_04391_b200", "libautomat.so")]
     libs += sorted(glob.glob(os.path.join(ROOT, "tools", "variants", "*", "libautomat.so")))
     for lib in libs:
-        subprocess.run([sys.executable, __file__, "--one", lib, n, its], check=False)
+        subprocess.run([sys.executable, __file__, "--one", lib, n, its, mode], check=False)
