@@ -152,7 +152,8 @@ int am_eval_batch_record_host(const am_law *law, const am_cfg *cfg, int64_t B,
  * rhs_strain_jacobian, gsm.py:574-602), evaluated by the same device AD
  * routines as the material kernel.  AoS host arrays: eps (B,6), a (B,m);
  * outputs sigma (B,6), A (B,m), f (B,m), dfda (B,m,m), dfde (B,m,6); any
- * output may be NULL.
+ * output may be NULL.  Automatic strategy only; am_lawops_host (below)
+ * covers every strategy and the tangents and is what the Python shim uses.
  */
 int am_constitutive_host(const am_law *law, int64_t B, const double *eps, const double *a,
                          double *sigma, double *A, double *f, double *dfda, double *dfde);
