@@ -750,7 +750,7 @@ AM_HD int tangent_point(const Law& L, const double* eps_n, const double* eps_np1
         const double r = step_strain(eps_n, eps_np1, dt, e1);
         int status = 0;
 #ifndef AM_TAN_BLOCK
-#define AM_TAN_BLOCK 6
+#define AM_TAN_BLOCK 3
 #endif
 #ifndef AM_TAN_COMBINED
 #define AM_TAN_COMBINED 1
@@ -802,10 +802,11 @@ AM_HD int tangent_point(const Law& L, const double* eps_n, const double* eps_np1
             for (int i = 0; i < m; ++i) x[i] = 0.0;
             if (!exact_solve(L, e1, a, h, x, false, true)) status |= ST_SINGULAR;
         }
-        // strain directions in blocks of AM_TAN_BLOCK columns
-        sfor<6 / AM_TAN_BLOCK>([&](auto Bk) {
-            tangent_block<decltype(Bk)::value * AM_TAN_BLOCK, AM_TAN_BLOCK>(L, e1, r, h, a, ac, eps_np1, fac, fast,
-                                                                            sig, sink);
+        // strain directions in blocks of columns (semi-automatic: 6, measured
+        // 1.20e9 vs 1.18e9 evals/s with 3)
+        constexpr int kBlk = is_semi_v<Law> ? 6 : AM_TAN_BLOCK;
+        sfor<6 / kBlk>([&](auto Bk) {
+            tangent_block<decltype(Bk)::value * kBlk, kBlk>(L, e1, r, h, a, ac, eps_np1, fac, fast, sig, sink);
         });
         return status;
         }
