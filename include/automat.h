@@ -172,8 +172,10 @@ typedef struct am_stepinfo {       /* homogenize.StepInfo (homogenize.py:337-342
     int32_t converged;
     double residual;               /* last history entry max(res, res_bc) */
     double mean_substeps;
-    double ebar[6];                /* mean strain of the returned (last evaluated) field */
-    double sig_bar[6];             /* mean stress of the returned field */
+    double ebar[6];                /* voxel mean of the returned (last evaluated) strain field,
+                                      eps.mean() of homogenize.py:503 (sums per x plane, added in
+                                      plane order: independent of the slab / GPU count) */
+    double sig_bar[6];             /* voxel mean of the returned stress field (same order) */
 } am_stepinfo;
 
 enum { AM_FIELD_EPS = 0, AM_FIELD_EPS_N = 1, AM_FIELD_SIGMA = 2 };
@@ -228,22 +230,30 @@ int am_solver_solve_step(am_solver *h, const double *ebar_target, double dt, con
  * agree with the cold start to round-off, not bit for bit.  No reference
  * counterpart (the reference always starts at a_n, odeint.py:371). */
 int am_solver_set_warm_start(am_solver *h, int on);
-/* Homogenizer.commit_step (homogenize.py:474-480) for the solver's eps */
+/* Homogenizer.commit_step (homogenize.py:474-480) for the solver's eps:
+ * eps_n <- eps, ebar_n <- ebar and, if a solve_step converged since the
+ * last commit, the internal state <- that step's state (evaluations in
+ * between do not change what is committed) */
 int am_solver_commit(am_solver *h, const double *ebar);
 /* Homogenizer.evaluate_field (homogenize.py:389-421) of the device eps,
- * without tangent: sigma field and pending states */
+ * without tangent: sigma field; states to the evaluation slot
+ * (am_solver_get_state pending = 2) */
 int am_solver_evaluate(am_solver *h, double dt);
 /* evaluate_field(want_tangent=True) fused with reference_update
  * (homogenize.py:509-513): Cbar (36, optional) = voxel mean of C,
  * lam_mu (2, optional) = reference_update(C field); C_out (optional, host
- * (N, 6, 6)) receives the tangent field itself. */
+ * (N, 6, 6)) receives the tangent field itself.  C is reduced per (phase,
+ * x plane, part) and summed in that order: Cbar does not depend on the slab
+ * or GPU count.  States go to the evaluation slot. */
 int am_solver_tangent_sweep(am_solver *h, double dt, double *Cbar, double *lam_mu, double *C_out);
 /* host (6, nx_local, ny, nz): the whole grid for handles from
  * am_solver_create[_slabs], the rank's slab for am_solver_create_nccl */
 int am_solver_get_field(am_solver *h, int which, double *out);
 int am_solver_set_field(am_solver *h, int which, const double *in);
-/* per-phase internal state, host (count, m); pending = 1 for the state of
- * the last evaluation, 0 for the committed one (VoxelGrid.state) */
+/* per-phase internal state, host (count, m); pending = 0 for the committed
+ * state (VoxelGrid.state), 1 for the state of the last converged
+ * solve_step, 2 for the state of the last am_solver_evaluate /
+ * am_solver_tangent_sweep */
 int am_solver_get_state(am_solver *h, int phase, int pending, double *out);
 int am_solver_set_state(am_solver *h, int phase, const double *in);
 int am_solver_phase_count(am_solver *h, int phase, int64_t *count);

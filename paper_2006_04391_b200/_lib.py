@@ -36,6 +36,7 @@ VOXEL_NEWTON_FAILED = 1
 VOXEL_SINGULAR = 2
 VOXEL_NONFINITE = 4
 VOXEL_INTEGRATION = 8
+VOXEL_RADIAL = 16
 ERROR_MEASURE_CODES = {"internal": 0, "stress": 1}
 
 
@@ -192,12 +193,14 @@ def make_law(law):
     from .gsm import LinearElastic, MichelSuquet
 
     s = am_law()
-    if isinstance(law, MichelSuquet):
+    # exact types: a subclass may override omega / psi / clamp_state, which the
+    # device potentials would silently ignore
+    if type(law) is MichelSuquet:
         p = law.params
         s.kind = AM_LAW_MICHEL_SUQUET
         s.E, s.nu, s.sigma_Y, s.H = p.E, p.nu, p.sigma_Y, p.H
         s.eps0_dot, s.sigma_d, s.n = p.eps0_dot, p.sigma_d, p.n
-    elif isinstance(law, LinearElastic):
+    elif type(law) is LinearElastic:
         s.kind = AM_LAW_LINEAR_ELASTIC
         s.E, s.nu = law.E, law.nu
     else:

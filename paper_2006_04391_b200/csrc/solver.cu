@@ -166,10 +166,25 @@ __global__ void __launch_bounds__(kRedThreads, AM_FOURIER_MINB) k_fourier(Spec s
     if (threadIdx.x == 0) red[(int64_t)ky * kParts + part] = t;
 }
 
+// per-(x plane, component) sums of a slab field f (6, nxl, ny, nz) ->
+// out[(x0 + x) * 6 + c]: fixed per-thread strides and a fixed tree, so the
+// host's plane-ordered sum (field_means) is independent of the slab count
+__global__ void __launch_bounds__(kRedThreads) k_plane_sums(const double* __restrict__ f, int64_t Nl, int64_t plane,
+                                                            int x0, double* __restrict__ out) {
+    __shared__ double sh[kRedThreads / 32];
+    const int x = blockIdx.x, c = blockIdx.y;
+    const double* p = f + c * Nl + (int64_t)x * plane;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < plane; i += blockDim.x) acc += p[i];
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) out[(int64_t)(x0 + x) * 6 + c] = t;
+}
+
 // red[P*ny + 0..5] = Re S(origin) on the origin's owner (else 0),
 // red[P*ny + 6] = 1 if a material point's Newton failed, [7] = 1 if an
 // adaptive integration hit a cap, [8] = accepted substeps of the adaptive
-// kernels in the sweep, [9] = 0 (summed over slabs: all exact)
+// kernels in the sweep, [9] = 1 if a radial return stalled (summed over
+// slabs: all exact)
 __global__ void k_finish(const double2* __restrict__ S, int64_t cs, int owner, const uint32_t* __restrict__ flags,
                          const unsigned long long* __restrict__ subs, double* __restrict__ red, int64_t off) {
     const int c = threadIdx.x;
@@ -177,7 +192,7 @@ __global__ void k_finish(const double2* __restrict__ S, int64_t cs, int owner, c
     if (c == 6) red[off + 6] = (flags && (*flags & AM_VOXEL_NEWTON_FAILED)) ? 1.0 : 0.0;
     if (c == 7) red[off + 7] = (flags && (*flags & AM_VOXEL_INTEGRATION)) ? 1.0 : 0.0;
     if (c == 8) red[off + 8] = subs ? (double)*subs : 0.0;
-    if (c == 9) red[off + 9] = 0.0;
+    if (c == 9) red[off + 9] = (flags && (*flags & AM_VOXEL_RADIAL)) ? 1.0 : 0.0;
 }
 
 // origin bin of the update: ehat(0) = N ebar, inverse-FFT input ebar
@@ -318,19 +333,22 @@ __global__ void k_isotropic(RefMat ref, const double* __restrict__ e, double* __
     }
 }
 
-// K5: per-voxel tangent bounds + C sums over a chunk of tangents stored
-// C[(i*6+j)*cs + b].  Per block: [sum C (36), min kappa, max kappa,
-// min mu_lo, max mu_hi, non-finite count] -> stats[blockIdx * 41 + ...]
+// K5: per-voxel tangent bounds + C sums over tangents stored
+// C[(i*6+j)*cs + b], b = first, first + step, ... < end.  Block results:
+// sums[0..35] = sum C, sums[36] = non-finite count; mins[0..3] = min kappa,
+// -max kappa, min mu_lo, -max mu_hi (all four combine by min, in any order)
 constexpr int kStat = 41;
-__global__ void __launch_bounds__(kRedThreads) k_refstats(const double* __restrict__ C, int64_t cs, int64_t B,
-                                                          DevBasis db, double* __restrict__ stats) {
+constexpr int kSum = 37;
+constexpr int kSParts = 16;  // blocks per (phase, x plane) in the tangent sweep statistics
+__device__ void refstats_block(const double* __restrict__ C, int64_t cs, int64_t first, int64_t step, int64_t end,
+                               const DevBasis& db, double* __restrict__ sums, double* __restrict__ mins) {
     __shared__ double sh[kRedThreads / 32];
     __shared__ double red[kRedThreads];
     double sum[36];
 #pragma unroll
     for (int i = 0; i < 36; ++i) sum[i] = 0.0;
     double kmin = INFINITY, kmax = -INFINITY, mlo = INFINITY, mhi = -INFINITY, bad = 0.0;
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t b = first; b < end; b += step) {
         double c[6][6];
         bool fin = true;
 #pragma unroll
@@ -352,15 +370,13 @@ __global__ void __launch_bounds__(kRedThreads) k_refstats(const double* __restri
         mlo = fmin(mlo, lo);
         mhi = fmax(mhi, hi);
     }
-    double* out = stats + (int64_t)blockIdx.x * kStat;
 #pragma unroll
     for (int i = 0; i < 36; ++i) {
         const double t = block_sum(sum[i], sh);
-        if (threadIdx.x == 0) out[i] = t;
+        if (threadIdx.x == 0) sums[i] = t;
     }
     const double t = block_sum(bad, sh);
-    if (threadIdx.x == 0) out[40] = t;
-    // min / max are order independent
+    if (threadIdx.x == 0) sums[36] = t;
     const double vals[4] = {kmin, -kmax, mlo, -mhi};
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
@@ -370,9 +386,40 @@ __global__ void __launch_bounds__(kRedThreads) k_refstats(const double* __restri
             if (threadIdx.x < s) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + s]);
             __syncthreads();
         }
-        if (threadIdx.x == 0) out[36 + v] = (v & 1) ? -red[0] : red[0];
+        if (threadIdx.x == 0) mins[v] = red[0];
         __syncthreads();
     }
+}
+
+// reference_update of a stored tangent field: grid-stride blocks, record
+// b at stats[b * kStat] = [sums (37) | mins (4)]
+__global__ void __launch_bounds__(kRedThreads) k_refstats(const double* __restrict__ C, int64_t cs, int64_t B,
+                                                          DevBasis db, double* __restrict__ stats) {
+    double* out = stats + (int64_t)blockIdx.x * kStat;
+    refstats_block(C, cs, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, B, db, out,
+                   out + kSum);
+}
+
+// tangent sweep chunk = x planes [xa, xa + gridDim.x / kSParts) of one phase;
+// block (plane, part) reduces part `part` of the plane's voxels (gidx range
+// poff[x] .. poff[x + 1], chunk-relative by `base`) into record
+// (plane, part) at sums[rec * kSum] / mins[rec * 4].  Records are indexed by
+// the global plane, so their plane-ordered sum does not depend on the chunk
+// size, the slab count or the GPU count.
+__global__ void __launch_bounds__(kRedThreads) k_refstats_planes(const double* __restrict__ C, int64_t cs,
+                                                                 const int64_t* __restrict__ poff, int xa,
+                                                                 int64_t base, DevBasis db, double* __restrict__ sums,
+                                                                 double* __restrict__ mins) {
+    const int x = xa + blockIdx.x / kSParts, part = blockIdx.x % kSParts;
+    const int64_t p0 = poff[x] - base, n = poff[x + 1] - poff[x];
+    const int64_t lo = p0 + n * part / kSParts, hi = p0 + n * (part + 1) / kSParts;
+    refstats_block(C, cs, lo + threadIdx.x, blockDim.x, hi, db, sums + (int64_t)blockIdx.x * kSum,
+                   mins + (int64_t)blockIdx.x * 4);
+}
+
+__global__ void k_fill(double* __restrict__ p, int64_t n, double v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
 }
 
 // ---------------------------------------------------------------- host helpers
@@ -434,13 +481,19 @@ struct Stats {
         kmax = mhi = -INFINITY;
         bad = 0.0;
     }
-    void add(const double* s) {
+    void add_sums(const double* s) {
         for (int i = 0; i < 36; ++i) Csum[i] += s[i];
-        kmin = std::fmin(kmin, s[36]);
-        kmax = std::fmax(kmax, s[37]);
-        mlo = std::fmin(mlo, s[38]);
-        mhi = std::fmax(mhi, s[39]);
-        bad += s[40];
+        bad += s[36];
+    }
+    void add_mins(const double* m) {
+        kmin = std::fmin(kmin, m[0]);
+        kmax = std::fmax(kmax, -m[1]);
+        mlo = std::fmin(mlo, m[2]);
+        mhi = std::fmax(mhi, -m[3]);
+    }
+    void add(const double* s) {  // one k_refstats record
+        add_sums(s);
+        add_mins(s + kSum);
     }
 };
 
@@ -451,7 +504,10 @@ struct Phase {
     int64_t count = 0;        // voxels of this phase in the slab
     int64_t* gidx = nullptr;  // slab-local voxel indices (sorted)
     double* a_n = nullptr;
-    double* a_pend = nullptr;
+    double* a_pend = nullptr;  // state of the last converged solve_step (committed by am_solver_commit)
+    double* a_tmp = nullptr;   // state of the last evaluation: basic-scheme iterates, evaluate, tangent sweep
+    std::vector<int64_t> poff; // gidx range of slab x-plane x: [poff[x], poff[x + 1])
+    int64_t* dpoff = nullptr;  // device copy
 };
 
 struct Slab {
@@ -497,6 +553,11 @@ struct am_solver {
     double* stats = nullptr;
     double* hstats = nullptr;
     double* dsmall = nullptr;     // nccl reductions of the tangent statistics
+    double* pl = nullptr;         // per-plane sums of eps and sigma (2 x nx x 6), field_means
+    double* hpl = nullptr;        // pinned host copy
+    int64_t nstat = 0;            // tangent statistics records: nmat x nx x kSParts
+    double* ps = nullptr;         // per-(phase, x plane, part) records of k_refstats_planes
+    double* hps = nullptr;        // pinned host copy
     bool p2p = false;             // fused pack / unpack over peer memory instead of the all-to-all
     std::vector<void*> ipc_open;  // peer buffers opened with cudaIpcOpenMemHandle
     double lam = 0.0, mu = 0.0;
@@ -520,6 +581,8 @@ static void solver_free(am_solver* h) {
             cudaFree(p.gidx);
             cudaFree(p.a_n);
             cudaFree(p.a_pend);
+            cudaFree(p.a_tmp);
+            cudaFree(p.dpoff);
         }
         cudaFree(s.eps); cudaFree(s.eps_n); cudaFree(s.sigma);
         cudaFree(s.S); cudaFree(s.ehat); cudaFree(s.P); cudaFree(s.X); cudaFree(s.flags); cudaFree(s.subs);
@@ -527,6 +590,7 @@ static void solver_free(am_solver* h) {
     }
     cudaFree(h->red); cudaFreeHost(h->hred);
     cudaFree(h->Cbuf); cudaFree(h->status); cudaFree(h->stats); cudaFreeHost(h->hstats); cudaFree(h->dsmall);
+    cudaFree(h->pl); cudaFreeHost(h->hpl); cudaFree(h->ps); cudaFreeHost(h->hps);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     for (cufftHandle p : {h->r3, h->c3, h->r2, h->c2, h->x1})
@@ -634,9 +698,9 @@ static int inverse(am_solver* h, double2* Slab::*src, double* Slab::*field) {
     return AM_OK;
 }
 
-// K1 over every phase of every local slab
-// warm: start each voxel's Newton from its pending state (the previous
-// basic-scheme iterate) instead of a_n (am_solver_set_warm_start)
+// K1 over every phase of every local slab; states -> a_tmp
+// warm: start each voxel's Newton from a_tmp (the previous basic-scheme
+// iterate) instead of a_n (am_solver_set_warm_start)
 static int material_sweep(am_solver* h, double dt, bool warm = false) {
     for (auto& s : h->slabs) {
         AM_CUDA(cudaMemsetAsync(s.flags, 0, sizeof(uint32_t), h->stream));
@@ -648,9 +712,9 @@ static int material_sweep(am_solver* h, double dt, bool warm = false) {
             k.B = p.count;
             k.gidx = p.gidx;
             k.eps_n = s.eps_n; k.eps_np1 = s.eps; k.a_n = p.a_n; k.dt = nullptr; k.dt_scalar = dt;
-            k.a_start = (warm && p.m && h->cfg.integrator == AM_INTEGRATOR_IMPLICIT_EULER) ? p.a_pend : nullptr;
+            k.a_start = (warm && p.m && h->cfg.integrator == AM_INTEGRATOR_IMPLICIT_EULER) ? p.a_tmp : nullptr;
             k.le = {s.Nl, 1}; k.la = {p.count, 1}; k.lc = {0, 0};
-            k.sigma = s.sigma; k.a_out = p.a_pend; k.C = nullptr;
+            k.sigma = s.sigma; k.a_out = p.a_tmp; k.C = nullptr;
             k.iters = nullptr; k.status = nullptr; k.flags = s.flags;
             set_controls(k, &h->cfg);
             AM_TRY(launch_material(&p.law, k, h->stream));
@@ -697,6 +761,32 @@ static int fourier_pass_x(am_solver* h, std::vector<double>& out) {
     AM_CUDA(cudaGetLastError());
     out.resize(L);
     return reduce_to_host(h, out.data());
+}
+
+// voxel means of eps and sigma (homogenize.py:448, 503-504: numpy's mean over
+// the grid), as plane sums added in global plane order on the host
+static int field_means(am_solver* h, double* ebar, double* sbar) {
+    const int64_t L = (int64_t)h->nx * 6;
+    AM_CUDA(cudaMemsetAsync(h->pl, 0, sizeof(double) * 2 * L, h->stream));
+    const int64_t plane = (int64_t)h->ny * h->nz;
+    for (auto& s : h->slabs) {
+        k_plane_sums<<<dim3(s.nxl, 6), kRedThreads, 0, h->stream>>>(s.eps, s.Nl, plane, s.x0, h->pl);
+        k_plane_sums<<<dim3(s.nxl, 6), kRedThreads, 0, h->stream>>>(s.sigma, s.Nl, plane, s.x0, h->pl + L);
+        AM_CUDA(cudaGetLastError());
+    }
+    if (h->comm) AM_NCCL(ncclAllReduce(h->pl, h->pl, 2 * L, ncclDouble, ncclSum, h->comm, h->stream));
+    AM_CUDA(cudaMemcpyAsync(h->hpl, h->pl, sizeof(double) * 2 * L, cudaMemcpyDeviceToHost, h->stream));
+    AM_CUDA(cudaStreamSynchronize(h->stream));
+    for (int c = 0; c < 6; ++c) {
+        double e = 0.0, t = 0.0;
+        for (int x = 0; x < h->nx; ++x) {
+            e += h->hpl[x * 6 + c];
+            t += h->hpl[L + x * 6 + c];
+        }
+        ebar[c] = e / (double)h->N;
+        sbar[c] = t / (double)h->N;
+    }
+    return AM_OK;
 }
 
 }  // namespace am
@@ -770,14 +860,19 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
             p.count = (int64_t)idx[k].size();
             sl.phases.push_back(p);
             Phase& ph = sl.phases.back();
+            ph.poff.resize(nxl + 1);
+            for (int x = 0; x <= nxl; ++x)
+                ph.poff[x] = std::lower_bound(idx[k].begin(), idx[k].end(), (int64_t)x * ny * nz) - idx[k].begin();
             if (!ph.count) continue;
+            AMC(cudaMalloc(&ph.dpoff, sizeof(int64_t) * (nxl + 1)));
+            AMC(cudaMemcpy(ph.dpoff, ph.poff.data(), sizeof(int64_t) * (nxl + 1), cudaMemcpyHostToDevice));
             AMC(cudaMalloc(&ph.gidx, sizeof(int64_t) * ph.count));
             AMC(cudaMemcpy(ph.gidx, idx[k].data(), sizeof(int64_t) * ph.count, cudaMemcpyHostToDevice));
             if (ph.m) {
-                AMC(cudaMalloc(&ph.a_n, sizeof(double) * ph.m * ph.count));
-                AMC(cudaMalloc(&ph.a_pend, sizeof(double) * ph.m * ph.count));
-                AMC(cudaMemset(ph.a_n, 0, sizeof(double) * ph.m * ph.count));
-                AMC(cudaMemset(ph.a_pend, 0, sizeof(double) * ph.m * ph.count));
+                for (double** a : {&ph.a_n, &ph.a_pend, &ph.a_tmp}) {
+                    AMC(cudaMalloc(a, sizeof(double) * ph.m * ph.count));
+                    AMC(cudaMemset(*a, 0, sizeof(double) * ph.m * ph.count));
+                }
             }
         }
     }
@@ -794,12 +889,18 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
         if (law_m(&laws[ids[i]])) ++h->nstate;
     AMC(cudaMalloc(&h->red, sizeof(double) * h->redlen * h->slabs.size()));
     AMC(cudaMallocHost(&h->hred, sizeof(double) * h->redlen * h->slabs.size()));
-    h->chunk = std::min<int64_t>(Nl, int64_t(1) << 22);
+    // tangent sweep chunks are whole x planes of a phase: at least one plane
+    h->chunk = std::max<int64_t>(std::min<int64_t>(Nl, int64_t(1) << 22), (int64_t)ny * nz);
     AMC(cudaMalloc(&h->Cbuf, sizeof(double) * 36 * h->chunk));
     AMC(cudaMalloc(&h->status, h->chunk));
     AMC(cudaMalloc(&h->stats, sizeof(double) * kStat * kRedBlocks));
     AMC(cudaMallocHost(&h->hstats, sizeof(double) * kStat * kRedBlocks));
     AMC(cudaMalloc(&h->dsmall, sizeof(double) * 64));
+    AMC(cudaMalloc(&h->pl, sizeof(double) * 12 * nx));
+    AMC(cudaMallocHost(&h->hpl, sizeof(double) * 12 * nx));
+    h->nstat = (int64_t)nmat * nx * kSParts;
+    AMC(cudaMalloc(&h->ps, sizeof(double) * kStat * h->nstat));
+    AMC(cudaMallocHost(&h->hps, sizeof(double) * kStat * h->nstat));
 #undef AMC
     size_t ws = 0;
     auto plan = [&](cufftHandle* p, int rank, long long* n, long long* inembed, long long istride, long long idist,
@@ -1026,11 +1127,12 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
             AM_TRY(acc(2, 3, 2));
             h->t_ms[4] += 1.0;
         }
-        if (o[P + 6] != 0.0 || o[P + 7] != 0.0) {
+        if (o[P + 6] != 0.0 || o[P + 7] != 0.0 || o[P + 9] != 0.0) {
             info->iterations = it;
             if (o[P + 6] != 0.0)
                 return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel (iteration %d)", it);
-            return fail(AM_ERR_INTEGRATION, "adaptive integration hit a cap (iteration %d)", it);
+            if (o[P + 7] != 0.0) return fail(AM_ERR_INTEGRATION, "adaptive integration hit a cap (iteration %d)", it);
+            return fail(AM_ERR_RADIAL, "radial return stalled for at least one voxel (iteration %d)", it);
         }
         // Homogenizer's mean substeps (homogenize.py:420-421): implicit Euler,
         // frozen points and laws without state take one substep per voxel
@@ -1059,6 +1161,11 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
         }
         if (res < tol && res_bc < tol) {  // strict (homogenize.py:454)
             info->converged = 1;
+            AM_TRY(field_means(h, info->ebar, info->sig_bar));
+            // the converged evaluation's state becomes the pending state
+            // (homogenize.py:455-457); earlier evaluations never touch it
+            for (auto& s : h->slabs)
+                for (auto& p : s.phases) std::swap(p.a_pend, p.a_tmp);
             h->pending = true;
             return AM_OK;
         }
@@ -1117,119 +1224,139 @@ extern "C" int am_solver_commit(am_solver* h, const double* ebar) {
     return AM_OK;
 }
 
-// material evaluation of the current eps field (Homogenizer.evaluate_field,
-// homogenize.py:389-421) without tangent: sigma field + pending states
-extern "C" int am_solver_evaluate(am_solver* h, double dt) {
-    if (!h) return fail(AM_ERR_ARG, "null solver");
-    AM_CUDA(cudaSetDevice(h->device));
-    AM_TRY(material_sweep(h, dt));
-    double bad = 0.0;
+// any per-voxel failure bit of the last sweep (OR over local slabs and ranks)
+static int sweep_flags(am_solver* h, uint32_t* any) {
+    uint32_t a = 0;
     for (auto& s : h->slabs) {
         uint32_t f = 0;
         AM_CUDA(cudaMemcpyAsync(&f, s.flags, sizeof(f), cudaMemcpyDeviceToHost, h->stream));
         AM_CUDA(cudaStreamSynchronize(h->stream));
-        if (f & AM_VOXEL_NEWTON_FAILED) bad = 1.0;
-        else if ((f & AM_VOXEL_INTEGRATION) && bad == 0.0) bad = 0.5;
+        a |= f;
     }
     if (h->comm) {
-        AM_CUDA(cudaMemcpyAsync(h->dsmall, &bad, sizeof(double), cudaMemcpyHostToDevice, h->stream));
-        AM_NCCL(ncclAllReduce(h->dsmall, h->dsmall, 1, ncclDouble, ncclMax, h->comm, h->stream));
-        AM_CUDA(cudaMemcpyAsync(&bad, h->dsmall, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        double v[5] = {0, 0, 0, 0, 0};
+        const uint32_t bits[5] = {AM_VOXEL_NEWTON_FAILED, AM_VOXEL_SINGULAR, AM_VOXEL_NONFINITE, AM_VOXEL_INTEGRATION,
+                                  AM_VOXEL_RADIAL};
+        for (int i = 0; i < 5; ++i) v[i] = (a & bits[i]) ? 1.0 : 0.0;
+        AM_CUDA(cudaMemcpyAsync(h->dsmall, v, sizeof(v), cudaMemcpyHostToDevice, h->stream));
+        AM_NCCL(ncclAllReduce(h->dsmall, h->dsmall, 5, ncclDouble, ncclMax, h->comm, h->stream));
+        AM_CUDA(cudaMemcpyAsync(v, h->dsmall, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
         AM_CUDA(cudaStreamSynchronize(h->stream));
+        a = 0;
+        for (int i = 0; i < 5; ++i)
+            if (v[i] > 0.0) a |= bits[i];
     }
-    h->pending = true;
-    if (bad == 1.0) return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
-    if (bad != 0.0) return fail(AM_ERR_INTEGRATION, "adaptive integration hit a cap");
+    *any = a;
     return AM_OK;
+}
+
+// the exception the reference raises first for a sweep's failure bits
+static int sweep_error(uint32_t any) {
+    if (any & AM_VOXEL_NEWTON_FAILED) return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
+    if (any & AM_VOXEL_INTEGRATION) return fail(AM_ERR_INTEGRATION, "adaptive integration hit a cap");
+    if (any & AM_VOXEL_RADIAL) return fail(AM_ERR_RADIAL, "radial return stalled for at least one voxel");
+    return AM_OK;
+}
+
+// material evaluation of the current eps field (Homogenizer.evaluate_field,
+// homogenize.py:389-421) without tangent: sigma field, states -> a_tmp.
+// The pending state of the last solve_step is not touched.
+extern "C" int am_solver_evaluate(am_solver* h, double dt) {
+    if (!h) return fail(AM_ERR_ARG, "null solver");
+    AM_CUDA(cudaSetDevice(h->device));
+    AM_TRY(material_sweep(h, dt));
+    uint32_t any = 0;
+    AM_TRY(sweep_flags(h, &any));
+    return sweep_error(any);
 }
 
 // Tangent sweep of the current eps from the committed state (the
 // evaluate_field(want_tangent=True) of run_loading_path, homogenize.py:509)
 // fused with reference_update (homogenize.py:307-329): C is produced in
-// chunks and reduced to C_bar (36) and the spectral bounds; it is stored
-// only if C_out (host, (N_local, 6, 6) in voxel order of the local slabs)
-// is given.  Also refreshes sigma and the pending states.
+// chunks of whole x planes and reduced per (phase, plane, part) to C_bar
+// (36) and the spectral bounds; it is stored only if C_out (host,
+// (N_local, 6, 6) in voxel order of the local slabs) is given.  Refreshes
+// sigma; states -> a_tmp (the pending state of solve_step is kept, as the
+// reference commits solve_step's state, homogenize.py:508-512).
 extern "C" int am_solver_tangent_sweep(am_solver* h, double dt, double* Cbar, double* lam_mu, double* C_out) {
     if (!h) return fail(AM_ERR_ARG, "null solver");
     AM_CUDA(cudaSetDevice(h->device));
-    Stats st;
-    st.reset();
-    uint32_t any = 0;
+    const int64_t ns = h->nstat;
+    double* dsum = h->ps;             // ns x kSum
+    double* dmin = h->ps + ns * kSum; // ns x 4
+    AM_CUDA(cudaMemsetAsync(dsum, 0, sizeof(double) * ns * kSum, h->stream));
+    k_fill<<<grid_for(ns * 4), 256, 0, h->stream>>>(dmin, ns * 4, INFINITY);
+    AM_CUDA(cudaGetLastError());
     std::vector<double> hC;
     std::vector<int64_t> hidx;
     int64_t vbase = 0;
     for (auto& s : h->slabs) {
         AM_CUDA(cudaMemsetAsync(s.flags, 0, sizeof(uint32_t), h->stream));
-        for (auto& p : s.phases) {
+        for (size_t ip = 0; ip < s.phases.size(); ++ip) {
+            Phase& p = s.phases[ip];
             if (!p.count) continue;
             if (C_out) {
                 hidx.resize(p.count);
                 AM_CUDA(cudaMemcpy(hidx.data(), p.gidx, sizeof(int64_t) * p.count, cudaMemcpyDeviceToHost));
             }
-            for (int64_t lo = 0; lo < p.count; lo += h->chunk) {
-                const int64_t n = std::min(h->chunk, p.count - lo);
-                KArgs k{};
-                k.B = n;
-                k.gidx = p.gidx + lo;
-                k.eps_n = s.eps_n; k.eps_np1 = s.eps;
-                k.a_n = p.m ? p.a_n + lo : nullptr;
-                k.dt = nullptr; k.dt_scalar = dt;
-                k.le = {s.Nl, 1}; k.la = {p.count, 1}; k.lc = {n, 1};
-                k.sigma = s.sigma; k.a_out = p.m ? p.a_pend + lo : nullptr; k.C = h->Cbuf;
-                k.iters = nullptr; k.status = h->status; k.flags = s.flags;
-                set_controls(k, &h->cfg);
-                AM_TRY(launch_material(&p.law, k, h->stream));
-                k_refstats<<<kRedBlocks, kRedThreads, 0, h->stream>>>(h->Cbuf, n, n, h->db, h->stats);
-                AM_CUDA(cudaGetLastError());
-                AM_CUDA(cudaMemcpyAsync(h->hstats, h->stats, sizeof(double) * kStat * kRedBlocks,
-                                        cudaMemcpyDeviceToHost, h->stream));
-                if (C_out) {
-                    hC.resize((size_t)36 * n);
-                    AM_CUDA(cudaMemcpyAsync(hC.data(), h->Cbuf, sizeof(double) * 36 * n, cudaMemcpyDeviceToHost,
-                                            h->stream));
+            for (int xa = 0; xa < s.nxl;) {
+                int xb = xa + 1;  // planes [xa, xb): as many as fit the chunk
+                while (xb < s.nxl && p.poff[xb + 1] - p.poff[xa] <= h->chunk) ++xb;
+                const int64_t lo = p.poff[xa], n = p.poff[xb] - lo;
+                if (n > 0) {
+                    KArgs k{};
+                    k.B = n;
+                    k.gidx = p.gidx + lo;
+                    k.eps_n = s.eps_n; k.eps_np1 = s.eps;
+                    k.a_n = p.m ? p.a_n + lo : nullptr;
+                    k.dt = nullptr; k.dt_scalar = dt;
+                    k.le = {s.Nl, 1}; k.la = {p.count, 1}; k.lc = {n, 1};
+                    k.sigma = s.sigma; k.a_out = p.m ? p.a_tmp + lo : nullptr; k.C = h->Cbuf;
+                    k.iters = nullptr; k.status = h->status; k.flags = s.flags;
+                    set_controls(k, &h->cfg);
+                    AM_TRY(launch_material(&p.law, k, h->stream));
+                    const int64_t rec = ((int64_t)ip * h->nx + s.x0 + xa) * kSParts;
+                    k_refstats_planes<<<(unsigned)((xb - xa) * kSParts), kRedThreads, 0, h->stream>>>(
+                        h->Cbuf, n, p.dpoff, xa, lo, h->db, dsum + rec * kSum, dmin + rec * 4);
+                    AM_CUDA(cudaGetLastError());
+                    if (C_out) {
+                        hC.resize((size_t)36 * n);
+                        AM_CUDA(cudaMemcpyAsync(hC.data(), h->Cbuf, sizeof(double) * 36 * n, cudaMemcpyDeviceToHost,
+                                                h->stream));
+                        AM_CUDA(cudaStreamSynchronize(h->stream));
+                        for (int64_t b = 0; b < n; ++b)
+                            for (int e = 0; e < 36; ++e)
+                                C_out[(vbase + hidx[lo + b]) * 36 + e] = hC[(size_t)e * n + b];
+                    }
                 }
-                AM_CUDA(cudaStreamSynchronize(h->stream));
-                for (int b = 0; b < kRedBlocks; ++b) st.add(h->hstats + (size_t)b * kStat);
-                if (C_out)
-                    for (int64_t b = 0; b < n; ++b)
-                        for (int e = 0; e < 36; ++e) C_out[(vbase + hidx[lo + b]) * 36 + e] = hC[(size_t)e * n + b];
+                xa = xb;
             }
         }
-        uint32_t f = 0;
-        AM_CUDA(cudaMemcpy(&f, s.flags, sizeof(f), cudaMemcpyDeviceToHost));
-        any |= f;
         vbase += s.Nl;
     }
     if (h->comm) {
-        // combine across ranks: sums (C, bad, flags) and extremes
-        double v[48];
-        for (int i = 0; i < 36; ++i) v[i] = st.Csum[i];
-        v[36] = st.bad;
-        v[37] = (any & AM_VOXEL_NEWTON_FAILED) ? 1.0 : 0.0;
-        v[38] = (any & AM_VOXEL_SINGULAR) ? 1.0 : 0.0;
-        v[39] = (any & AM_VOXEL_NONFINITE) ? 1.0 : 0.0;
-        v[44] = (any & AM_VOXEL_INTEGRATION) ? 1.0 : 0.0;
-        v[40] = st.kmin; v[41] = -st.kmax; v[42] = st.mlo; v[43] = -st.mhi;
-        AM_CUDA(cudaMemcpyAsync(h->dsmall, v, sizeof(v), cudaMemcpyHostToDevice, h->stream));
-        AM_NCCL(ncclAllReduce(h->dsmall, h->dsmall, 40, ncclDouble, ncclSum, h->comm, h->stream));
-        AM_NCCL(ncclAllReduce(h->dsmall + 40, h->dsmall + 40, 4, ncclDouble, ncclMin, h->comm, h->stream));
-        AM_NCCL(ncclAllReduce(h->dsmall + 44, h->dsmall + 44, 1, ncclDouble, ncclSum, h->comm, h->stream));
-        AM_CUDA(cudaMemcpyAsync(v, h->dsmall, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
-        AM_CUDA(cudaStreamSynchronize(h->stream));
-        for (int i = 0; i < 36; ++i) st.Csum[i] = v[i];
-        st.bad = v[36];
-        any = (v[37] > 0.0 ? AM_VOXEL_NEWTON_FAILED : 0u) | (v[38] > 0.0 ? AM_VOXEL_SINGULAR : 0u) |
-              (v[39] > 0.0 ? AM_VOXEL_NONFINITE : 0u) | (v[44] > 0.0 ? AM_VOXEL_INTEGRATION : 0u);
-        st.kmin = v[40]; st.kmax = -v[41]; st.mlo = v[42]; st.mhi = -v[43];
+        // records are disjoint across ranks (zero / +inf where not owned)
+        AM_NCCL(ncclAllReduce(dsum, dsum, ns * kSum, ncclDouble, ncclSum, h->comm, h->stream));
+        AM_NCCL(ncclAllReduce(dmin, dmin, ns * 4, ncclDouble, ncclMin, h->comm, h->stream));
     }
-    h->pending = true;
-    if (any & AM_VOXEL_NEWTON_FAILED) return fail(AM_ERR_NEWTON, "implicit Euler Newton failed for at least one voxel");
-    if (any & AM_VOXEL_INTEGRATION) return fail(AM_ERR_INTEGRATION, "adaptive integration hit a cap");
+    AM_CUDA(cudaMemcpyAsync(h->hps, h->ps, sizeof(double) * ns * kStat, cudaMemcpyDeviceToHost, h->stream));
+    AM_CUDA(cudaStreamSynchronize(h->stream));
+    uint32_t any = 0;
+    AM_TRY(sweep_flags(h, &any));
+    Stats st;
+    st.reset();
+    for (int64_t r = 0; r < ns; ++r) {  // fixed order: phase, global x plane, part
+        st.add_sums(h->hps + r * kSum);
+        st.add_mins(h->hps + ns * kSum + r * 4);
+    }
+    AM_TRY(sweep_error(any));
     if (Cbar)
         for (int i = 0; i < 36; ++i) Cbar[i] = st.Csum[i] / (double)h->N;
+    // the tangent LU raises inside evaluate_field (odeint.py:424), before
+    // reference_update sees the field (homogenize.py:316-317)
+    if (any & AM_VOXEL_SINGULAR) return fail(AM_ERR_SINGULAR, "pivot below 1e-14 * max|A| in the tangent LU");
     if (st.bad > 0.0 || (any & AM_VOXEL_NONFINITE))
         return fail(AM_ERR_NONFINITE, "tangent field contains non-finite entries");
-    if (any & AM_VOXEL_SINGULAR) return fail(AM_ERR_SINGULAR, "pivot below 1e-14 * max|A| in the tangent LU");
     if (lam_mu) {
         const double mu_ref = 0.5 * (st.mlo + st.mhi);
         const double kappa_ref = 0.5 * (st.kmin + st.kmax);
@@ -1271,7 +1398,8 @@ extern "C" int am_solver_set_field(am_solver* h, int which, const double* in) {
 }
 
 // per-phase state, host (count, m) in voxel order over the local slabs;
-// pending = 0 committed, 1 pending
+// pending = 0 committed, 1 pending (last converged solve_step), 2 the last
+// evaluation (evaluate / tangent sweep)
 static int state_copy(am_solver* h, int phase, int pending, double* host, bool to_host) {
     if (!h || phase < 0 || phase >= (int)h->slabs[0].phases.size()) return fail(AM_ERR_ARG, "bad phase");
     AM_CUDA(cudaSetDevice(h->device));
@@ -1281,7 +1409,7 @@ static int state_copy(am_solver* h, int phase, int pending, double* host, bool t
         const Phase& p = s.phases[phase];
         if (p.m && p.count) {
             std::vector<double> soa((size_t)p.m * p.count);
-            double* dp = pending ? p.a_pend : p.a_n;
+            double* dp = pending == 2 ? p.a_tmp : pending ? p.a_pend : p.a_n;
             if (to_host) {
                 AM_CUDA(cudaMemcpy(soa.data(), dp, sizeof(double) * soa.size(), cudaMemcpyDeviceToHost));
                 for (int64_t b = 0; b < p.count; ++b)

@@ -310,7 +310,6 @@ class Homogenizer:
             _lib.check(self._lib.am_solver_ipc_import(h, b"".join(every), comm.world), "ipc import")
         self._ebar_n = np.zeros(6)
         self._last = None  # (eps, ebar) host arrays of the last converged step
-        self._pending = False
         if comm is None:
             self._push_state(grid._state)
             grid._solver = self
@@ -409,12 +408,10 @@ class Homogenizer:
         """One material evaluation per voxel from the committed state (homogenize.py:389-421).
 
         Returns (sigma_field, C (N, 6, 6) or None, state list, mean substeps).
+        The evaluation's state goes to a device scratch slot: the pending
+        state of the last solve_step, which commit_step commits, is untouched
+        (homogenize.py:399-421, 474-480).
         """
-        if self._pending:
-            # keep the converged step's pending state: this sweep overwrites it
-            held = [np.empty((len(i), law.m)) for i, law in zip(self.grid.voxel_index, self.grid.materials)]
-            self._pull_state(held, pending=True)
-            self._pending = held
         self._set(0, eps_np1_field)
         self._last = None
         C = None
@@ -425,7 +422,7 @@ class Homogenizer:
             _lib.check(self._lib.am_solver_evaluate(self._h, float(dt)), "evaluate_field")
         sigma = self._get(2)
         state = [np.empty((len(i), law.m)) for i, law in zip(self.grid.voxel_index, self.grid.materials)]
-        self._pull_state(state, pending=True)
+        self._pull_state(state, pending=2)
         return sigma, C, state, 1.0
 
     # -- one loading step ------------------------------------------------------
@@ -445,7 +442,6 @@ class Homogenizer:
                 history,
             )
         _lib.check(rc, "solve_step")
-        self._pending = True
         return info, history
 
     def solve_step(self, ebar_target, dt, free_mask=None):
@@ -457,16 +453,12 @@ class Homogenizer:
                                     history=history)
 
     def commit_step(self, eps, ebar):
-        """eps_n <- eps, ebar_n <- ebar, internal state <- pending (homogenize.py:474-480)."""
+        """eps_n <- eps, ebar_n <- ebar, internal state <- the state of the last
+        converged solve_step, if any (homogenize.py:474-480)."""
         if self._last is None or eps is not self._last[0]:
             self._set(0, eps)
-        if isinstance(self._pending, list):
-            for i, arr in enumerate(self._pending):
-                if self.grid.materials[i].m and len(arr):
-                    _lib.check(self._lib.am_solver_set_state(self._h, i, _lib.ptr(np.ascontiguousarray(arr))))
         self._ebar_n = np.array(ebar, dtype=float)
         _lib.check(self._lib.am_solver_commit(self._h, _lib.ptr(self._ebar_n)))
-        self._pending = False
         self._last = None
 
 
@@ -506,7 +498,6 @@ def run_loading_path(grid, path, cfg, update_reference=True, threads=1, tol=1e-5
         else:
             hom._ebar_n = ebar
             _lib.check(lib.am_solver_commit(hom._h, _lib.ptr(ebar)))
-        hom._pending = False
         if k == len(times) - 1 and comm is None:
             hom.grid.state  # noqa: B018  (refresh the host copy of the final state)
         records.append({

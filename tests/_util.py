@@ -29,3 +29,28 @@ def rowwise_relerr(x, y):
 def assert_close(x, y, tol, what=""):
     e = relerr(x, y)
     assert e <= tol, f"{what}: relative error {e:.3e} > {tol:.1e}"
+
+
+def check_path_records(recs, g, what, parity_log=None):
+    """Loading-path records against a reference fixture: identical
+    iteration counts, sigma_bar / eps_bar within 1e-10 (per step, each
+    record scaled by its own magnitude), C_bar / reference materials within
+    TOL_TANGENT.  Returns the measured errors."""
+    k = len(g["iterations"])
+    recs = recs[:k]
+    assert [r["iterations"] for r in recs] == g["iterations"].tolist(), what
+    sig = np.stack([r["sig"] for r in recs])
+    errs = {
+        "steps": k,
+        "sig_bar": float(rowwise_relerr(sig, g["sig"]).max()),
+        "sig_xx": float(np.max(np.abs(sig[:, 0] - g["sig"][:, 0]) / np.abs(g["sig"][:, 0]))),
+        "eps_xx": float(np.max(np.abs(np.array([r["eps_xx"] for r in recs]) - g["eps_xx"]) / np.abs(g["eps_xx"]))),
+        "C11": float(np.max(np.abs(np.array([r["C11"] for r in recs]) - g["C11"]) / np.abs(g["C11"]))),
+        "C12": float(np.max(np.abs(np.array([r["C12"] for r in recs]) - g["C12"]) / np.abs(g["C12"]))),
+    }
+    if parity_log is not None:
+        parity_log(what, **errs)
+    assert errs["sig_bar"] <= TOL_STATE and errs["sig_xx"] <= TOL_STATE and errs["eps_xx"] <= TOL_STATE, (what, errs)
+    assert errs["C11"] <= TOL_TANGENT and errs["C12"] <= TOL_TANGENT, (what, errs)
+    assert all(r["mean_substeps"] == 1.0 for r in recs)
+    return errs

@@ -31,6 +31,7 @@ from gsmkit import homogenize as H  # noqa: E402
 from gsmkit.evaluator import StrategyConfig, evaluate_arrays  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+OUT = os.environ.get("GOLD_OUT", HERE)  # long runs write elsewhere first
 _spec = importlib.util.spec_from_file_location(
     "workloads", os.path.join(HERE, "..", "..", "paper_2006_04391_b200", "workloads.py")
 )
@@ -85,7 +86,7 @@ def eval_counted(law, cfg, eps_n, a_n, eps_np1, dt, want_tangent):
 
 
 def save(name, **arrays):
-    path = os.path.join(HERE, name)
+    path = os.path.join(OUT, name)
     np.savez_compressed(path, **arrays)
     print(f"wrote {name} ({os.path.getsize(path) / 1024:.1f} KiB)")
 
@@ -495,11 +496,120 @@ def make_path16_conv():
     save("path16_conv.npz", **arr)
 
 
+def make_path_conv(n, steps=20):
+    """n^3 toy MMC, LoadingPath(steps), per-law conventional oracle (SURVEY
+    §8c, App. C): the same call sequence as the reference's run_loading_path
+    (homogenize.py:485-528), written out so the Homogenizer stays reachable
+    for per-step histories, reference materials and final field samples.
+    The fixture is rewritten after every step, so a long run (128^3: hours)
+    pins every step it has finished."""
+    _ea = H.evaluate_arrays
+
+    def _per_law(law, cfg, *a, **k):
+        if cfg.strategy == "conventional" and not law.has_conventional:
+            cfg = AUTO
+        return _ea(law, cfg, *a, **k)
+
+    H.evaluate_arrays = _per_law
+    try:
+        _path_by_hand(n, CONV, f"path{n}_conv.npz", steps)
+    finally:
+        H.evaluate_arrays = _ea
+
+
+def make_path8_ode23():
+    """8^3 toy MMC, first 3 of the default LoadingPath()'s 80 steps with the
+    DEFAULT StrategyConfig()
+    (automatic, ode23): the tangent sweep of run_loading_path is a coupled
+    adaptive integration with its own step sequence, and the state committed
+    must be solve_step's (homogenize.py:508-512)."""
+    _path_by_hand(8, StrategyConfig(), "path8_ode23.npz", 80, last=3)
+
+
+def make_path8_ode23_fail():
+    """The same with LoadingPath(steps=20): step 1 converges, step 2 raises
+    SolverError after 5000 iterations (the adaptive integrator's tolerance
+    keeps the residual above 1e-5); fixture = step-1 records + the history."""
+    grid = H.toy_mmc_grid(8)
+    hom = H.Homogenizer(grid, StrategyConfig())
+    path = H.LoadingPath(steps=20)
+    t = path.times()
+    free = np.array([False, True, True, True, True, True])
+    out = {}
+    for k in (1, 2):
+        eb = np.zeros(6)
+        eb[0] = path.eps_xx(t[k])
+        try:
+            eps, sigma, info = hom.solve_step(eb, t[k] - t[k - 1], free_mask=free)
+        except H.SolverError as exc:
+            out["fail_step"] = np.array(k)
+            out["fail_history"] = np.array(exc.history)
+            break
+        out[f"step{k}_iters"] = np.array(info.iterations)
+        out[f"step{k}_sig"] = sigma.mean(axis=(1, 2, 3))
+        _, C_vox, _, _ = hom.evaluate_field(eps, t[k] - t[k - 1], want_tangent=True)
+        hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+        hom.set_reference(H.reference_update(C_vox))
+    save("path8_ode23_fail.npz", **out)
+
+
+def _path_by_hand(n, cfg, name, steps, last=None):
+    """The reference's run_loading_path sequence (homogenize.py:485-528) by hand."""
+    t0 = time.time()
+    grid = H.toy_mmc_grid(n)
+    path = H.LoadingPath(steps=steps)
+    hom = H.Homogenizer(grid, cfg)
+    times = path.times()
+    targets = path.eps_xx(times)
+    free = np.array([False, True, True, True, True, True]) if path.mixed_bc else np.zeros(6, dtype=bool)
+    recs, hist, refs = [], [], [(hom.reference.lam, hom.reference.mu)]
+    rng = np.random.default_rng(7)
+    sub = np.sort(rng.choice(n**3, size=min(4096, n**3), replace=False))
+    for k in range(1, (last or steps) + 1):
+        dt = times[k] - times[k - 1]
+        eb = np.zeros(6)
+        eb[0] = targets[k]
+        eps, sigma, info = hom.solve_step(eb, dt, free_mask=free)
+        ebar = eps.mean(axis=(1, 2, 3))
+        sig_bar = sigma.mean(axis=(1, 2, 3))
+        _, C_vox, _, _ = hom.evaluate_field(eps, dt, want_tangent=True)
+        C_bar = C_vox.mean(axis=0)
+        hom.commit_step(eps, ebar)
+        hom.set_reference(H.reference_update(C_vox))
+        refs.append((hom.reference.lam, hom.reference.mu))
+        recs.append({"step": k, "time": float(times[k]), "eps_xx": float(ebar[0]), "sig": sig_bar.copy(),
+                     "C11": float(C_bar[0, 0]), "C12": float(C_bar[0, 1]), "iterations": info.iterations,
+                     "mean_substeps": info.mean_substeps, "Cbar": C_bar, "ebar": ebar})
+        hist.append(np.array(info.history))
+        del C_vox
+        arr = _records_to_arrays(recs)
+        arr["Cbar"] = np.stack([r["Cbar"] for r in recs])
+        arr["ebar"] = np.stack([r["ebar"] for r in recs])
+        arr["history_flat"] = np.concatenate(hist)
+        arr["refs"] = np.array(refs)
+        arr["ids"] = grid.material_ids
+        arr["sub"] = sub
+        # converged fields of the last finished step, sampled
+        arr["eps_sub"] = eps.reshape(6, -1)[:, sub]
+        arr["sig_sub"] = sigma.reshape(6, -1)[:, sub]
+        # committed matrix state (material 0, m = 7) at the sampled voxels
+        st = np.zeros((n**3, grid.materials[0].m))
+        st[grid.voxel_index[0]] = grid.state[0]
+        arr["state_sub"] = st[sub].T.copy()
+        arr["seconds"] = np.array(time.time() - t0)
+        save(name, **arr)
+        print(f"{name} step {k}: {info.iterations} it ({time.time() - t0:.1f}s)", flush=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
     ap.add_argument("--only", default="")
+    ap.add_argument("--path-n", type=int, default=0, help="run make_path_conv(n) only")
     args = ap.parse_args()
+    if args.path_n:
+        make_path_conv(args.path_n)
+        sys.exit(0)
     jobs = {
         "material": make_material,
         "adaptive": make_adaptive,
@@ -510,11 +620,15 @@ if __name__ == "__main__":
         "config1": make_config1,
         "path16": make_path16_conv,
         "path8": make_path8,
+        "path8_ode23": make_path8_ode23,
+        "path8_ode23_fail": make_path8_ode23_fail,
+        "path32": lambda: make_path_conv(32),
+        "path64": lambda: make_path_conv(64),
     }
     for name, fn in jobs.items():
         if args.only and name not in args.only.split(","):
             continue
-        if args.skip_slow and name in ("path8",):
+        if args.skip_slow and name in ("path8", "path8_ode23", "path8_ode23_fail", "path32", "path64"):
             continue
         t0 = time.time()
         fn()

@@ -9,6 +9,7 @@ quantities within 1e-8 relative.
 import numpy as np
 import pytest
 
+from _util import check_path_records, rowwise_relerr
 from conftest import golden
 from oracle import homogenize as OH
 from oracle import material as OM
@@ -131,21 +132,161 @@ def test_path8_manual_loop(H, AUTO):
     assert rel(grid.state[0], g["state0"]) < TOL
 
 
+def _path_fixture(n):
+    import os
+
+    from conftest import GOLDEN
+
+    f = os.path.join(GOLDEN, f"path{n}_conv.npz")
+    if not os.path.exists(f):
+        pytest.skip(f"no reference fixture for the {n}^3 path")
+    return np.load(f)
+
+
 @pytest.mark.parametrize("warm", [False, True])
-def test_run_loading_path_16(H, AUTO, warm):
-    """Full 20-step path at 16^3: identical iteration counts
-    (also with the Newton warm start, which changes per-voxel Newton counts only)."""
-    g = golden("path16_conv.npz")
-    grid = H.toy_mmc_grid(16)
+@pytest.mark.parametrize("n", [16, 32, 64, 128])
+def test_run_loading_path(H, AUTO, n, warm, parity_log):
+    """Full 20-step path at n^3 vs the reference (per-law conventional route,
+    SURVEY §8c / App. A.2b; identical counts to the automatic route at 16^3):
+    identical iteration counts, also with the Newton warm start (which
+    changes per-voxel Newton counts only)."""
+    g = _path_fixture(n)
+    grid = H.toy_mmc_grid(n)
     assert np.array_equal(grid.material_ids, g["ids"])
     recs = H.run_loading_path(grid, H.LoadingPath(steps=20), AUTO, newton_warm_start=warm)
-    assert [r["iterations"] for r in recs] == g["iterations"].tolist()
-    sig = np.stack([r["sig"] for r in recs])
-    assert rel(sig[:, 0], g["sig"][:, 0]) < 1e-9
-    assert rel([r["C11"] for r in recs], g["C11"]) < 1e-8
-    assert rel([r["C12"] for r in recs], g["C12"]) < 1e-8
-    assert rel([r["eps_xx"] for r in recs], g["eps_xx"]) < 1e-9
-    assert all(r["mean_substeps"] == 1.0 for r in recs)
+    check_path_records(recs, g, f"path{n}{'_warm' if warm else ''}", parity_log)
+    if len(g["iterations"]) == 20 and not warm:
+        # committed state and strain of the last step at the sampled voxels
+        sub = g["sub"]
+        st = np.zeros((n**3, 7))
+        st[grid.voxel_index[0]] = grid.state[0]
+        e_state = float(rowwise_relerr(st[sub], g["state_sub"].T).max())
+        parity_log(f"path{n}_final_state", state=e_state)
+        assert e_state <= TOL
+
+
+def test_path_manual_loop_32(H, AUTO, parity_log):
+    """The reference's per-step sequence through the public Homogenizer API
+    at 32^3 (first 4 steps): per-step histories, full C_bar, reference
+    materials and eps.mean() as the committed mean strain."""
+    g = _path_fixture(32)
+    grid = H.toy_mmc_grid(32)
+    hom = H.Homogenizer(grid, AUTO)
+    path = H.LoadingPath(steps=20)
+    times = path.times()
+    targets = path.eps_xx(times)
+    free = np.array([False, True, True, True, True, True])
+    hist = np.split(g["history_flat"], np.cumsum(g["iterations"])[:-1])
+    worst = dict(hist=0.0, ebar=0.0, Cbar=0.0, ref=0.0)
+    for k in range(1, 5):
+        dt = times[k] - times[k - 1]
+        eb = np.zeros(6)
+        eb[0] = targets[k]
+        eps, sigma, info = hom.solve_step(eb, dt, free_mask=free)
+        assert info.iterations == g["iterations"][k - 1]
+        worst["hist"] = max(worst["hist"], rel(info.history, hist[k - 1]))
+        ebar = eps.mean(axis=(1, 2, 3))
+        worst["ebar"] = max(worst["ebar"], rel(ebar, g["ebar"][k - 1]))
+        _, C_vox, _, _ = hom.evaluate_field(eps, dt, want_tangent=True)
+        worst["Cbar"] = max(worst["Cbar"], rel(C_vox.mean(axis=0), g["Cbar"][k - 1]))
+        hom.commit_step(eps, ebar)
+        hom.set_reference(H.reference_update(C_vox))
+        worst["ref"] = max(worst["ref"], rel([hom.reference.lam, hom.reference.mu], g["refs"][k]))
+    parity_log("path32_manual", **worst)
+    assert worst["hist"] < 1e-8 and worst["ebar"] < TOL and worst["Cbar"] < 1e-8 and worst["ref"] < 1e-8, worst
+
+
+def test_commit_keeps_solve_step_state(H, AUTO):
+    """commit_step commits the state of the last converged solve_step, not
+    that of a later evaluate_field at another strain (homogenize.py:455-457,
+    474-480); without a solve_step nothing is committed."""
+    grid = H.toy_mmc_grid(8)
+    hom = H.Homogenizer(grid, AUTO)
+    free = np.array([False] + [True] * 5)
+    eb = np.array([2e-3, 0, 0, 0, 0, 0])
+    eps, sigma, info = hom.solve_step(eb, 0.4, free_mask=free)
+    _, _, state_conv, _ = hom.evaluate_field(eps, 0.4)
+    s2, C2, state_pert, _ = hom.evaluate_field(1.5 * eps, 0.4, want_tangent=True)
+    assert rel(state_pert[0], state_conv[0]) > 1e-3  # the perturbed evaluation differs
+    hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+    assert rel(grid.state[0], state_conv[0]) == 0.0
+    assert rel(hom.eps_n, eps) == 0.0
+    # evaluate_field alone, then commit: the committed state stays
+    before = grid.state[0].copy()
+    hom.evaluate_field(2.0 * eps, 0.4)
+    hom.commit_step(2.0 * eps, 2.0 * eps.mean(axis=(1, 2, 3)))
+    assert rel(grid.state[0], before) == 0.0
+    assert rel(hom.eps_n, 2.0 * eps) == 0.0
+
+
+def test_path8_default_cfg_ode23(H):
+    """First 3 steps of the 8^3 path with the default StrategyConfig()
+    (automatic, ode23) against the reference: the per-step tangent sweep is
+    a coupled adaptive integration with its own step sequence, and the
+    committed state must still be solve_step's (homogenize.py:508-512)."""
+    import os
+
+    from conftest import GOLDEN
+    from paper_2006_04391_b200.evaluator import StrategyConfig
+
+    f = os.path.join(GOLDEN, "path8_ode23.npz")
+    if not os.path.exists(f):
+        pytest.skip("no ode23 path fixture")
+    g = np.load(f)
+    grid = H.toy_mmc_grid(8)
+    hom = H.Homogenizer(grid, StrategyConfig())
+    path = H.LoadingPath()  # 80 steps (homogenize.py:52-77)
+    times = path.times()
+    free = np.array([False] + [True] * 5)
+    for k in range(1, 4):
+        dt = times[k] - times[k - 1]
+        eb = np.zeros(6)
+        eb[0] = path.eps_xx(times[k])
+        eps, sigma, info = hom.solve_step(eb, dt, free_mask=free)
+        assert info.iterations == g["iterations"][k - 1]
+        assert info.mean_substeps == pytest.approx(g["mean_substeps"][k - 1], rel=1e-12)
+        assert rel(sigma.mean(axis=(1, 2, 3)), g["sig"][k - 1]) < TOL
+        ebar = eps.mean(axis=(1, 2, 3))
+        _, C_vox, _, _ = hom.evaluate_field(eps, dt, want_tangent=True)
+        assert rel(C_vox.mean(axis=0), g["Cbar"][k - 1]) < 1e-8
+        hom.commit_step(eps, ebar)
+        hom.set_reference(H.reference_update(C_vox))
+        assert rel([hom.reference.lam, hom.reference.mu], g["refs"][k]) < 1e-8
+    st = np.zeros((512, 7))
+    st[grid.voxel_index[0]] = grid.state[0]
+    assert float(rowwise_relerr(st[g["sub"]], g["state_sub"].T).max()) <= TOL
+
+
+def test_path8_default_cfg_ode23_solver_error(H, parity_log):
+    """LoadingPath(steps=20) with the default StrategyConfig(): the reference
+    converges step 1 and raises SolverError in step 2 after 5000 iterations
+    (ode23's error control keeps the residual above tol); so must this."""
+    from paper_2006_04391_b200.evaluator import StrategyConfig
+
+    g = golden("path8_ode23_fail.npz")
+    grid = H.toy_mmc_grid(8)
+    hom = H.Homogenizer(grid, StrategyConfig())
+    path = H.LoadingPath(steps=20)
+    t = path.times()
+    free = np.array([False] + [True] * 5)
+    eb = np.zeros(6)
+    eb[0] = path.eps_xx(t[1])
+    eps, sigma, info = hom.solve_step(eb, t[1], free_mask=free)
+    assert info.iterations == int(g["step1_iters"])
+    assert rel(sigma.mean(axis=(1, 2, 3)), g["step1_sig"]) < TOL
+    _, C_vox, _, _ = hom.evaluate_field(eps, t[1], want_tangent=True)
+    hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+    hom.set_reference(H.reference_update(C_vox))
+    eb[0] = path.eps_xx(t[2])
+    with pytest.raises(H.SolverError) as ei:
+        hom.solve_step(eb, t[2] - t[1], free_mask=free)
+    hist, ref = np.array(ei.value.history), g["fail_history"]
+    assert len(hist) == len(ref) == 5000
+    # the residual sequence follows the reference's until the adaptive step
+    # controller's discrete decisions amplify round-off
+    agree = int(np.argmax(np.abs(hist - ref) > 1e-6 * np.abs(ref))) or len(ref)
+    parity_log("path8_ode23_fail", history_agree=agree, last=float(hist[-1]), ref_last=float(ref[-1]))
+    assert agree >= 20
 
 
 @pytest.mark.parametrize("slabs", [1, 2])

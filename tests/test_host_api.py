@@ -107,3 +107,38 @@ def test_lawops_strategy_validation():
         gsm.evolution_rhs(law, np.zeros(6), np.zeros(7), strategy="numeric")
     with pytest.raises(ValueError):
         gsm.conventional_evaluate(gsm.LinearElastic(1e9, 0.3), np.zeros(6), np.zeros(0), np.zeros(6), 0.1)
+
+
+def test_law_subclass_has_no_device_potentials():
+    """A subclass may override the potentials: it must not run on the built-in
+    device laws (ConfigError, no CPU fallback)."""
+    from paper_2006_04391_b200 import _lib, gsm
+    from paper_2006_04391_b200.evaluator import ConfigError
+
+    class Stiffer(gsm.LinearElastic):
+        def omega(self, eps, a):  # pragma: no cover - never evaluated
+            return 2.0 * super().omega(eps, a)
+
+    assert _lib.make_law(gsm.LinearElastic(1e9, 0.3)).kind == _lib.AM_LAW_LINEAR_ELASTIC
+    assert _lib.make_law(gsm.MichelSuquet()).kind == _lib.AM_LAW_MICHEL_SUQUET
+    with pytest.raises(ConfigError):
+        _lib.make_law(Stiffer(1e9, 0.3))
+
+
+def test_loading_path_fixtures_are_consistent():
+    """The n^3 path fixtures (reference, per-law conventional route) share the
+    loading times and geometry generator with this package."""
+    import os
+
+    from conftest import GOLDEN
+    from paper_2006_04391_b200 import homogenize as H
+
+    t = H.LoadingPath(steps=20).times()
+    for n in (16, 32, 64, 128):
+        f = os.path.join(GOLDEN, f"path{n}_conv.npz")
+        if not os.path.exists(f):
+            continue
+        g = np.load(f)
+        k = len(g["iterations"])
+        np.testing.assert_array_equal(t[1:k + 1], g["time"])
+        assert np.array_equal(H.toy_mmc_grid(n).material_ids, g["ids"])

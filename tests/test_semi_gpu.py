@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from conftest import golden
-from _util import TOL_STATE, TOL_TANGENT, assert_close
+from _util import TOL_STATE, TOL_TANGENT, assert_close, check_path_records
 
 pytestmark = pytest.mark.gpu
 
@@ -66,9 +66,7 @@ def test_semi_path16(api):
     g = golden("path16_conv.npz")
     cfg = SC(strategy="semi-automatic", integrator="implicit-euler")
     recs = H.run_loading_path(H.toy_mmc_grid(16), H.LoadingPath(steps=20), cfg)
-    assert [r["iterations"] for r in recs] == g["iterations"].tolist()
-    assert_close([r["sig"][0] for r in recs], g["sig"][:, 0], 1e-9)
-    assert_close([r["C11"] for r in recs], g["C11"], 1e-8)
+    check_path_records(recs, g, "path16_semi")
 
 
 @pytest.mark.parametrize("tang", [False, True])
