@@ -6,6 +6,7 @@ It restates gsmkit/homogenize.py step by step:
 
 * ``green_matrix``        GreenOperator._assemble + Nyquist/origin rules (homogenize.py:184-227)
 * ``green_apply``         GreenOperator.apply (homogenize.py:229-233)
+* ``green_apply_slabwise`` the same with the table built per kx slab (512^3 checks)
 * ``residual``            equilibrium_residual (homogenize.py:241-267)
 * ``iso``                 apply_isotropic (homogenize.py:270-281)
 * ``reference_update``    reference_update with the Mandel / deviatoric basis (homogenize.py:288-329)
@@ -71,6 +72,42 @@ def green_apply(tau, lam, mu, G=None):
     G = green_matrix(dims, lam, mu) if G is None else G
     th = np.fft.rfftn(tau, axes=(1, 2, 3))
     return np.fft.irfftn(-np.einsum("pqxyz,qxyz->pxyz", G, th), s=dims, axes=(1, 2, 3))
+
+
+def green_apply_slabwise(tau, lam, mu, kx_chunk=16):
+    """green_apply with the Green table built kx-slab by kx-slab (the full
+    (6, 6, nx, ny, nz/2+1) table is 18 GiB at 512^3); same formulas and
+    Nyquist / origin rules as green_matrix (homogenize.py:184-233)."""
+    dims = tau.shape[1:]
+    nx, ny, nz = dims
+    fx, fy, fz = _freqs(dims)
+    c1 = 1.0 / (4.0 * mu)
+    c2 = (lam + mu) / (mu * (lam + 2.0 * mu))
+    Cinv = np.linalg.inv(iso_matrix(lam, mu))
+    nyq_y = np.abs(np.abs(fy) - ny / 2.0) < 1e-9
+    nyq_z = np.abs(np.abs(fz) - nz / 2.0) < 1e-9
+    th = np.fft.rfftn(tau, axes=(1, 2, 3))
+    for x0 in range(0, nx, kx_chunk):
+        x1 = min(nx, x0 + kx_chunk)
+        xi = np.stack(np.meshgrid(fx[x0:x1], fy, fz, indexing="ij"))
+        nrm = np.sqrt((xi**2).sum(axis=0))
+        if x0 == 0:
+            nrm[0, 0, 0] = 1.0
+        n = xi / nrm
+        out = np.zeros((6,) + n.shape[1:], dtype=complex)
+        nyq = ((np.abs(np.abs(fx[x0:x1]) - nx / 2.0) < 1e-9)[:, None, None] | nyq_y[None, :, None]
+               | nyq_z[None, None, :])
+        for p, (k, h) in enumerate(VOIGT):
+            for q, (i, j) in enumerate(VOIGT):
+                t = c1 * ((k == i) * n[h] * n[j] + (h == i) * n[k] * n[j] + (k == j) * n[h] * n[i]
+                          + (h == j) * n[k] * n[i])
+                G = (2.0 if p > 2 else 1.0) * (2.0 if q > 2 else 1.0) * (t - c2 * n[i] * n[j] * n[k] * n[h])
+                G[nyq] = Cinv[p, q]
+                if x0 == 0:
+                    G[0, 0, 0] = 0.0
+                out[p] -= G * th[q, x0:x1]
+        th[:, x0:x1] = out
+    return np.fft.irfftn(th, s=dims, axes=(1, 2, 3))
 
 
 def residual(sig):

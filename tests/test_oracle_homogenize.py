@@ -69,3 +69,13 @@ def test_path8_first_steps():
         np.testing.assert_allclose([r["lam"], r["mu"]], g["refs"][k + 1], rtol=1e-13)
     np.testing.assert_allclose(b.eps_n, g["eps_n"], rtol=0, atol=1e-12 * np.abs(g["eps_n"]).max())
     np.testing.assert_allclose(b.state[0], g["state0"], rtol=0, atol=1e-12 * np.abs(g["state0"]).max())
+
+
+def test_green_apply_slabwise_matches_table():
+    """The slab-wise Green application (512^3 checks) is the table version."""
+    rng = np.random.default_rng(5)
+    for dims in [(16, 12, 10), (9, 8, 7), (8, 6, 5)]:
+        tau = rng.normal(0, 1e8, (6,) + dims)
+        a = OH.green_apply(tau, 8e10, 7e10)
+        b = OH.green_apply_slabwise(tau, 8e10, 7e10, kx_chunk=3)
+        assert np.max(np.abs(a - b)) <= 1e-14 * np.max(np.abs(a))
