@@ -156,103 +156,178 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def basic_scheme(n, lib, dev, dist=None, warm=False):
-    """Basic-scheme iterations/s on config 4's microstructure (toy_mmc_grid(n),
-    elasto-viscoplastic matrix + elastic fibre), load step 1 of
-    LoadingPath(steps=20) with mixed BCs, device-resident; per-phase times
-    from am_solver_timing (CUDA events on the solver stream).  Under torchrun
-    the grid is x-slab decomposed over the ranks (NCCL all-to-all transposes,
-    strong scaling); the time is the max over ranks."""
+FREE = np.array([False, True, True, True, True, True])
+
+
+def _solver_stream(hom, dev):
     import torch
 
-    from paper_2006_04391_b200 import distributed as D
+    from paper_2006_04391_b200 import _lib
+
+    sp = ctypes.c_void_p()
+    _lib.check(hom._lib.am_solver_stream(hom._h, ctypes.byref(sp)))
+    return torch.cuda.ExternalStream(sp.value, device=dev)
+
+
+def _max_over_ranks(dist, dev, x):
+    if dist is None:
+        return float(x)
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def basic_step(grid, n, dev, dist=None, comm=None, warm=False, max_iterations=5000, label=""):
+    """Basic-scheme iterations/s of load step 1 of LoadingPath(steps=20)
+    (mixed BC, tol 1e-5) on `grid`, device time (CUDA events on the solver
+    stream, max over ranks); per-phase times from am_solver_timing.  With
+    `comm` the grid is x-slab decomposed over the ranks (strong scaling).
+    max_iterations < the step's count times that many iterations (the
+    SolverError is expected and caught)."""
+    import torch
 
     from paper_2006_04391_b200 import _lib, homogenize as H
     from paper_2006_04391_b200.evaluator import StrategyConfig
 
     cfg = StrategyConfig(strategy="automatic", integrator="implicit-euler")
-    grid = H.toy_mmc_grid(n)
-    comm = D.comm_from_torch() if dist is not None else None
-    try:
-        hom = H.Homogenizer(grid, cfg, comm=comm, newton_warm_start=warm)
-        ok = 1
-    except Exception as exc:  # noqa: BLE001 - reported in the JSON line
-        hom, ok, why = None, 0, f"{type(exc).__name__}: {exc}"
-    if not agree(dist, dev, ok):
-        return {"metric": "basic-scheme iterations/s", "error": why if not ok else "setup failed on another rank"}
-    sp = ctypes.c_void_p()
-    _lib.check(lib.am_solver_stream(hom._h, ctypes.byref(sp)))
-    stream = torch.cuda.ExternalStream(sp.value, device=dev)
+    hom = H.Homogenizer(grid, cfg, comm=comm, newton_warm_start=warm, max_iterations=max_iterations)
+    lib = hom._lib
+    stream = _solver_stream(hom, dev)
     path = H.LoadingPath(steps=20)
     times = path.times()
     target = np.zeros(6)
     target[0] = path.eps_xx(times)[1]
-    free = np.array([False, True, True, True, True, True])
     _lib.check(lib.am_solver_timing(hom._h, 1, None))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    capped = False
     with Clocks(torch.cuda.current_device()) as clk:
         e0.record(stream)
-        info, _ = hom._solve(target, times[1] - times[0], free)
+        try:
+            info, _ = hom._solve(target, times[1] - times[0], FREE)
+            iters = info.iterations
+        except H.SolverError as exc:
+            if max_iterations >= 5000:
+                raise
+            iters, capped = len(exc.history), True
         e1.record(stream)
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = _max_over_ranks(dist, dev, e0.elapsed_time(e1))
     ph = np.zeros(5)
     _lib.check(lib.am_solver_timing(hom._h, -1, _lib.ptr(ph)))
-    iters = info.iterations
-    N = n ** 3
     world = comm.world if comm is not None else 1
     Nh = n * n * (n // 2 + 1) // world  # rfft bins per rank
     it_t = ph[4] or 1.0
     fourier_ms = ph[2] / it_t
     fourier_bytes = 4 * 96.0 * Nh  # read shat, ehat; write ehat, shat (complex128 x 6)
-    return {
-        "metric": "basic-scheme iterations/s", "value": iters / (ms * 1e-3), "unit": "it/s",
-        "config": {"workload": f"config 4 grid toy_mmc_grid({n}) (EVP matrix, VF 0.10 elastic fibre), "
-                               f"load step 1 of LoadingPath(steps=20), mixed BC, tol 1e-5, {world} GPU(s)",
-                   "parallelism": "single GPU (3-D cuFFT)" if world == 1 else
-                   f"x-slabs over {world} GPUs, NCCL all-to-all transposes (strong scaling)",
-                   "voxels": N, "evp_voxels": int(len(grid.voxel_index[0]))},
-        "iterations": iters, "ms_total": ms, "ms_per_iteration": ms / iters,
-        "phase_ms_per_iteration": {"material": ph[0] / it_t, "d2z": ph[1] / it_t, "fourier+reduce": fourier_ms,
-                                   "origin+z2d": ph[3] / max(it_t - 1, 1)},
+    out = {
+        "value": iters / (ms * 1e-3), "unit": "it/s", "iterations": iters, "ms_total": ms,
+        "ms_per_iteration": ms / iters,
+        "phase_ms_per_iteration": {"material": ph[0] / it_t, "forward_fft": ph[1] / it_t,
+                                   "fourier+reduce": fourier_ms, "origin+inverse_fft": ph[3] / max(it_t - 1, 1)},
         "fourier_roofline": {"bound": "hbm", "achieved": fourier_bytes / (fourier_ms * 1e-3) / 1e9,
                              "peak": hbm_peak(), "unit": "GB/s",
                              "frac": fourier_bytes / (fourier_ms * 1e-3) / 1e9 / hbm_peak(),
-                             "traffic_per_launch_algorithmic": fourier_bytes,
-                             "note": "k_fourier incl. the fixed-order reduction and the 64-byte D2H of the residual"},
+                             "traffic_per_launch_algorithmic": fourier_bytes},
         "clocks": clk.summary(),
     }
+    if capped:
+        out["note"] = f"first {iters} iterations of load step 1 (max_iterations cap; per-iteration rate)"
+    del hom
+    return out
 
 
-def loading_path_bench(n, dev, dist=None, steps=20, warm=False):
-    """Config 3: the full 20-step loading path (tension-compression, mixed BC,
-    reference update every step) on toy_mmc_grid(n) through the public
-    run_loading_path, device time on the solver stream via am_solver_timing
-    plus wall time of the whole call (tangent sweeps included)."""
+def loading_path_run(grid, dev, dist=None, comm=None, steps=20, warm=False):
+    """The public run_loading_path (tension-compression, mixed BC, reference
+    update per step) on `grid`: wall time of the whole call with device
+    synchronisation on both sides (host-driven loop: convergence tests and
+    tangent sweeps included), max over ranks."""
     import torch
 
-    from paper_2006_04391_b200 import distributed as D, homogenize as H
+    from paper_2006_04391_b200 import homogenize as H
     from paper_2006_04391_b200.evaluator import StrategyConfig
 
     cfg = StrategyConfig(strategy="automatic", integrator="implicit-euler")
-    grid = H.toy_mmc_grid(n)
-    comm = D.comm_from_torch() if dist is not None else None
     torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
     t0 = time.perf_counter()
     recs = H.run_loading_path(grid, H.LoadingPath(steps=steps), cfg, comm=comm, newton_warm_start=warm)
     torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
+    wall = _max_over_ranks(dist, dev, time.perf_counter() - t0)
     its = int(sum(r["iterations"] for r in recs))
-    return {"metric": "basic-scheme iterations/s over the loading path", "value": its / wall, "unit": "it/s",
-            "config": {"workload": f"config 3: toy_mmc_grid({n}), LoadingPath(steps={steps}), mixed BC, "
-                                   "reference update per step, run_loading_path (wall clock incl. tangent sweeps)"},
-            "seconds": wall, "iterations_total": its, "iterations_per_step": [r["iterations"] for r in recs],
+    return {"value": its / wall, "unit": "it/s", "seconds": wall, "iterations_total": its,
+            "iterations_per_step": [r["iterations"] for r in recs],
             "sig_xx_final": float(recs[-1]["sig"][0]), "C11_final": recs[-1]["C11"]}
+
+
+def oracle_basic_seconds_per_iteration(n, k=2):
+    """CPU reference arm of the basic scheme: the oracle's
+    (C restatement of the automatic route + numpy field step, all host
+    threads) seconds per iteration of load step 1 at n^3, k iterations."""
+    from oracle import homogenize as OH
+    from oracle import material as OM
+    from paper_2006_04391_b200 import homogenize as H
+
+    ids = H.toy_mmc_grid(n).material_ids
+    b = OH.Basic(ids, [OM.ALUMINUM, OM.law_params(0, 300e9, 0.25)], max_iterations=k,
+                 threads=os.cpu_count() or 1)
+    t, ex = OH.loading_times(20)
+    eb = np.zeros(6)
+    eb[0] = ex[1]
+    t0 = time.perf_counter()
+    try:
+        b.solve_step(eb, t[1], FREE)
+    except OH.NotConverged:
+        pass
+    return (time.perf_counter() - t0) / k
+
+
+def config1_run(dev):
+    """Config 1: 32^3 two-phase elastic sphere, one load step (strain BC and
+    mixed BC), Homogenizer.solve_step device time; the numpy oracle (CPU)
+    timed on the same step."""
+    import torch
+
+    from oracle import homogenize as OH
+    from oracle import material as OM
+    from paper_2006_04391_b200 import gsm, homogenize as H
+    from paper_2006_04391_b200.evaluator import StrategyConfig
+    from paper_2006_04391_b200.workloads import sphere_ids
+
+    cfg = StrategyConfig(strategy="automatic", integrator="implicit-euler")
+    ids = sphere_ids(32)
+    eb = np.zeros(6)
+    eb[0] = 1e-3
+    out = {"config": {"workload": "config 1: 32^3 two-phase elastic sphere (VF 0.2), one load step, tol 1e-5"}}
+    for tag, free in (("strain_bc", np.zeros(6, bool)), ("mixed_bc", FREE)):
+        best = None
+        for _ in range(3):
+            hom = H.Homogenizer(H.VoxelGrid(ids, [gsm.LinearElastic(55e9, 0.33), gsm.LinearElastic(300e9, 0.25)]),
+                                cfg)
+            stream = _solver_stream(hom, dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            info, _ = hom._solve(eb, 1.0, free)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+            del hom
+        ob = OH.Basic(ids, [OM.law_params(0, 55e9, 0.33), OM.law_params(0, 300e9, 0.25)])
+        t0 = time.perf_counter()
+        _, _, oit, _ = ob.solve_step(eb, 1.0, free)
+        cpu_s = time.perf_counter() - t0
+        out[tag] = {"iterations": info.iterations, "ms": best, "value": info.iterations / (best * 1e-3),
+                    "unit": "it/s", "oracle_iterations": oit,
+                    "cpu_baseline": {"seconds": cpu_s, "value": oit / cpu_s, "unit": "it/s", "cores": 1,
+                                     "kind": "port", "sample": "the same load step, numpy restatement (oracle/)"}}
+    return out
 
 
 def agree(dist, dev, ok):
@@ -282,8 +357,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=B_DEFAULT)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--basic", type=int, default=256, help="grid size n of the basic-scheme line (0: skip)")
-    ap.add_argument("--path", type=int, default=128, help="grid size n of the config-3 loading path (0: skip)")
+    ap.add_argument("--basic", type=int, default=256, help="config-4 grid size n (0: skip the basic scheme)")
+    ap.add_argument("--path", type=int, default=128, help="config-3 grid size n (0: skip)")
+    ap.add_argument("--big", type=int, default=512, help="config-5 grid size n (0: skip)")
+    ap.add_argument("--big-iterations", type=int, default=0,
+                    help="config-5 iterations timed on one GPU (0: 300; the full load step on >1 GPU)")
+    ap.add_argument("--no-strategies", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -294,6 +373,12 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+
+    if world > 1:
+        # communicator evidence in the driver's log (NCCL INIT lines), for
+        # torch's communicator and libautomat's slab communicator alike
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
     import torch
 
@@ -307,7 +392,7 @@ def main():
     torch.cuda.set_device(dev)
 
     from paper_2006_04391_b200 import _lib, gsm
-    from paper_2006_04391_b200.evaluator import StrategyConfig
+    from paper_2006_04391_b200.evaluator import StrategyConfig, evaluate_arrays
     from paper_2006_04391_b200.workloads import config2_batch
 
     lib = _lib.load()
@@ -347,7 +432,7 @@ def main():
     if int(d_fl.item()) != 0:
         raise RuntimeError(f"material kernel reported status flags {int(d_fl.item())}")
 
-    # ---- device-resident throughput (inputs in HBM; 552 MiB of I/O per step > 126 MB L2)
+    # ---- config 2, device-resident (inputs in HBM; 552 MiB of I/O per step > 126 MB L2)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         barrier()
@@ -359,11 +444,9 @@ def main():
         torch.cuda.synchronize()
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = _max_over_ranks(dist, dev, ms)
     value = world * B / (ms_max * 1e-3)
+    clocks = clk.summary()
 
     iters = d_it.cpu().numpy()
     fl = float(np.sum(flops_per_eval(iters.astype(np.float64))))
@@ -380,9 +463,10 @@ def main():
     # ---- the paper's strategy comparison on the same batch (stress + tangent,
     # device-resident): every strategy x integrator route the reference offers
     strategies = {}
-    for strat, integ in (("automatic", "implicit-euler"), ("semi-automatic", "implicit-euler"),
-                         ("conventional", "implicit-euler"), ("automatic", "ode12"), ("automatic", "ode23"),
-                         ("semi-automatic", "ode23"), ("semi-automatic", "ode23s")):
+    for strat, integ in (() if args.no_strategies else (
+            ("automatic", "implicit-euler"), ("semi-automatic", "implicit-euler"),
+            ("conventional", "implicit-euler"), ("automatic", "ode12"), ("automatic", "ode23"),
+            ("semi-automatic", "ode23"), ("semi-automatic", "ode23s"))):
         c2 = _lib.make_cfg(StrategyConfig(strategy=strat, integrator=integ))
 
         def run(c2=c2):
@@ -392,56 +476,66 @@ def main():
             if rc:
                 _lib.check(rc)
 
-        try:
+        run()
+        run()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(5):
             run()
-            run()
-            torch.cuda.synchronize()
-            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            f0.record(stream)
-            for _ in range(5):
-                run()
-            f1.record(stream)
-            torch.cuda.synchronize()
-            t_ms = f0.elapsed_time(f1) / 5
-            strategies[f"{strat}/{integ}"] = {
-                "evals_per_s": B / (t_ms * 1e-3), "ms": t_ms,
-                ("mean_newton_iters" if integ == "implicit-euler" else "mean_substeps"):
-                    float(d_it.double().mean().item())}
-        except Exception as exc:  # noqa: BLE001
-            strategies[f"{strat}/{integ}"] = {"error": f"{type(exc).__name__}: {exc}"}
+        f1.record(stream)
+        torch.cuda.synchronize()
+        t_ms = f0.elapsed_time(f1) / 5
+        strategies[f"{strat}/{integ}"] = {
+            "evals_per_s": B / (t_ms * 1e-3), "ms": t_ms,
+            ("mean_newton_iters" if integ == "implicit-euler" else "mean_substeps"): float(d_it.double().mean().item())}
     step()  # leave the headline route's outputs in the buffers
     torch.cuda.synchronize()
 
-    # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    # ---- end to end, headline: the reference's own call, evaluate_arrays,
+    # with the caller's plain (pageable) numpy arrays; results come back as
+    # numpy arrays.  Host->device and device->host copies inside the timed region.
+    def e2e_py():
+        return evaluate_arrays(law, cfg, en, an, ep, dt, want_tangent=True)
+
+    for _ in range(2):
+        r = e2e_py()
+    del r
+    e2e_steps = max(3, min(args.steps, 10))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        r = e2e_py()
+    e2e_s = _max_over_ranks(dist, dev, (time.perf_counter() - t0) / e2e_steps)
+    assert np.array_equal(r.newton_iters, iters), "evaluate_arrays disagrees with the device path"
+    del r
+    e2e_value = world * B / e2e_s
+
+    # the same through the C ABI with pinned host buffers (the copy ceiling of the path)
     pin = lambda shape, dtype=torch.float64: torch.empty(shape, dtype=dtype, pin_memory=True).numpy()  # noqa: E731
     h_en, h_an, h_ep, h_dt = pin((B, 6)), pin((B, 7)), pin((B, 6)), pin((B,))
     h_en[:], h_an[:], h_ep[:], h_dt[:] = en, an, ep, dt
     h_sig, h_a, h_C, h_it = pin((B, 6)), pin((B, 7)), pin((B, 6, 6)), pin((B,), torch.int32)
 
-    def e2e_step():
-        rc = lib.am_eval_batch_host(s_law, s_cfg, B, _lib.ptr(h_en), _lib.ptr(h_an), _lib.ptr(h_ep), _lib.ptr(h_dt),
-                                    1, _lib.ptr(h_sig), _lib.ptr(h_a), _lib.ptr(h_C), _lib.ptr(h_it, _lib._i32p), None,
-                                    None)
-        _lib.check(rc)
+    def e2e_abi():
+        _lib.check(lib.am_eval_batch_host(s_law, s_cfg, B, _lib.ptr(h_en), _lib.ptr(h_an), _lib.ptr(h_ep),
+                                          _lib.ptr(h_dt), 1, _lib.ptr(h_sig), _lib.ptr(h_a), _lib.ptr(h_C),
+                                          _lib.ptr(h_it, _lib._i32p), None, None))
 
     for _ in range(2):
-        e2e_step()
-    e2e_steps = max(3, min(args.steps, 10))
+        e2e_abi()
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        e2e_step()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * B / float(e2e_t.item())
-    # the PCIe ceiling of that path: the same bytes as plain concurrent
-    # pinned copies (H2D on one stream, D2H on another), no kernels
-    h2d_b = B * (6 + 7 + 6 + 1) * 8
-    d2h_b = B * (6 + 7 + 36) * 8 + B * 4
-    hin = torch.empty(h2d_b // 8, dtype=torch.float64, pin_memory=True)
-    hout = torch.empty(d2h_b // 8, dtype=torch.float64, pin_memory=True)
+        e2e_abi()
+    abi_value = world * B / _max_over_ranks(dist, dev, (time.perf_counter() - t0) / e2e_steps)
+    assert np.array_equal(h_it, iters), "e2e path disagrees with the device path"
+    # PCIe ceiling: the same bytes as plain concurrent pinned copies (H2D on
+    # one stream, D2H on another), no kernels
+    h2d = B * (6 + 7 + 6 + 1) * 8
+    d2h = B * (6 + 7 + 36) * 8 + B * (4 + 4 + 1)  # + Newton counts, rejected, status
+    hin = torch.empty(h2d // 8, dtype=torch.float64, pin_memory=True)
+    hout = torch.empty(d2h // 8, dtype=torch.float64, pin_memory=True)
     din, dout = torch.empty_like(hin, device=dev), torch.empty_like(hout, device=dev)
     s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
 
@@ -458,48 +552,94 @@ def main():
         copies()
     torch.cuda.synchronize()
     pcie_ceiling = B / ((time.perf_counter() - t0) / 3)
-    del hin, hout, din, dout
-    assert np.array_equal(h_it, iters), "e2e path disagrees with the device path"
-    h2d = B * (6 + 7 + 6 + 1) * 8
-    d2h = B * (6 + 7 + 36) * 8 + B * 4
-    clocks = clk.summary()
-    basic = path = None
-    if args.basic:
-        try:
-            basic = basic_scheme(args.basic, lib, dev, dist)
-        except Exception as exc:  # noqa: BLE001 - the headline line must still print
-            basic = {"metric": "basic-scheme iterations/s", "error": f"{type(exc).__name__}: {exc}"}
-    if args.path and (dist is None or "error" not in (basic or {})):
-        try:
-            path = loading_path_bench(args.path, dev, dist)
-        except Exception as exc:  # noqa: BLE001
-            path = {"metric": "basic-scheme iterations/s over the loading path", "error": f"{type(exc).__name__}: {exc}"}
+    del hin, hout, din, dout, h_en, h_an, h_ep, h_dt, h_sig, h_a, h_C, h_it
+    del d_en, d_an, d_ep, d_dt, d_sig, d_a, d_C, d_it, d_st
+    torch.cuda.empty_cache()
 
-    # the same runs with the solver's Newton warm start (opt-in, not in the
-    # reference: identical basic-scheme iteration counts, fields equal to
-    # round-off, fewer per-voxel Newton iterations)
+    # ---- basic scheme (configs 1, 3, 4, 5): first-class keys; a failure
+    # fails the bench (non-zero exit after the line)
+    from paper_2006_04391_b200 import distributed as D, homogenize as H
+
+    basic, errors = {}, []
+    comm_of = (lambda transport: D.comm_from_torch(transport=transport)) if dist is not None else (lambda t: None)
+    par = (lambda t: "single GPU (3-D cuFFT)" if world == 1 else
+           f"x-slabs over {world} GPUs, 2-D cuFFT + {'ncclAlltoAll' if t == 'nccl' else 'fused P2P pack/unpack over NVLink'}"
+           " transposes + 1-D cuFFT over x (strong scaling)")
     warm_note = ("Homogenizer(newton_warm_start=True): each voxel's Newton starts at its previous basic-scheme "
-                 "iterate instead of a_n (opt-in; same equations and tolerance, identical basic-scheme iterations)")
-    if basic is not None and "error" not in basic:
+                 "iterate instead of a_n (opt-in, not in the reference; same equations and tolerance, identical "
+                 "basic-scheme iterations)")
+
+    def guarded(key, fn):
         try:
-            bw = basic_scheme(args.basic, lib, dev, dist, warm=True)
-            basic["newton_warm_start"] = {k: bw[k] for k in ("value", "unit", "iterations", "ms_per_iteration",
-                                                             "phase_ms_per_iteration")}
-            basic["newton_warm_start"]["note"] = warm_note
-        except Exception as exc:  # noqa: BLE001
-            basic["newton_warm_start"] = {"error": f"{type(exc).__name__}: {exc}"}
-    if path is not None and "error" not in path:
-        try:
-            pw = loading_path_bench(args.path, dev, dist, warm=True)
-            path["newton_warm_start"] = {k: pw[k] for k in ("value", "unit", "seconds", "iterations_total",
-                                                            "sig_xx_final", "C11_final")}
-            path["newton_warm_start"]["note"] = warm_note
-        except Exception as exc:  # noqa: BLE001
-            path["newton_warm_start"] = {"error": f"{type(exc).__name__}: {exc}"}
+            basic[key] = fn()
+        except Exception as exc:  # noqa: BLE001 - reported, then the bench exits non-zero
+            basic[key] = {"error": f"{type(exc).__name__}: {exc}"}
+            errors.append(key)
+
+    if args.basic:
+        n = args.basic
+        grid4 = H.toy_mmc_grid(n)
+        wl4 = (f"config 4: toy_mmc_grid({n}) (EVP matrix, VF 0.10 elastic fibre), LoadingPath(steps=20), mixed BC, "
+               f"tol 1e-5, {world} GPU(s)")
+
+        def c4_step():
+            r = basic_step(grid4, n, dev, dist, comm_of("nccl"))
+            r["config"] = {"workload": wl4 + ", load step 1", "parallelism": par("nccl"), "voxels": n**3,
+                           "evp_voxels": int(len(grid4.voxel_index[0]))}
+            rw = basic_step(grid4, n, dev, dist, comm_of("nccl"), warm=True)
+            r["newton_warm_start"] = {k: rw[k] for k in ("value", "unit", "iterations", "ms_per_iteration",
+                                                         "phase_ms_per_iteration")}
+            r["newton_warm_start"]["note"] = warm_note
+            if world > 1:
+                rp = basic_step(grid4, n, dev, dist, comm_of("p2p"))
+                r["p2p_transport"] = {k: rp[k] for k in ("value", "unit", "iterations", "ms_per_iteration",
+                                                         "phase_ms_per_iteration")}
+            return r
+
+        def c4_path():
+            r = loading_path_run(grid4, dev, dist, comm_of("nccl"))
+            r["config"] = {"workload": wl4 + ", all 20 load steps through run_loading_path (reference update per "
+                                             "step, tangent sweeps included)", "parallelism": par("nccl")}
+            r["note"] = "20-step average: iterations of all steps / wall time of run_loading_path"
+            return r
+
+        guarded("config4_step1", c4_step)
+        guarded("config4_20_steps", c4_path)
+    if args.path:
+        grid3 = H.toy_mmc_grid(args.path)
+
+        def c3():
+            r = loading_path_run(grid3, dev, dist, comm_of("nccl"))
+            r["config"] = {"workload": f"config 3: toy_mmc_grid({args.path}), LoadingPath(steps=20), mixed BC, "
+                                       "reference update per step, run_loading_path", "parallelism": par("nccl")}
+            rw = loading_path_run(grid3, dev, dist, comm_of("nccl"), warm=True)
+            r["newton_warm_start"] = {k: rw[k] for k in ("value", "unit", "seconds", "iterations_total",
+                                                         "sig_xx_final", "C11_final")}
+            r["newton_warm_start"]["note"] = warm_note
+            return r
+
+        guarded("config3_path", c3)
+    if args.big:
+        n = args.big
+        grid5 = H.toy_mmc_grid(n, fiber_law=gsm.LinearElastic(3000e9, 0.25))
+        cap = 5000 if world > 1 else (args.big_iterations or 300)
+
+        def c5():
+            r = basic_step(grid5, n, dev, dist, comm_of("nccl"), max_iterations=cap)
+            r["config"] = {"workload": f"config 5: toy_mmc_grid({n}, fiber_law=LinearElastic(3000e9, 0.25)) "
+                                       f"(~55x contrast), load step 1 of LoadingPath(steps=20), mixed BC, tol 1e-5",
+                           "parallelism": par("nccl"), "voxels": n**3}
+            return r
+
+        guarded("config5_step1", c5)
+    if world == 1 and args.basic:
+        guarded("config1", lambda: config1_run(dev))
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
+        if errors:
+            sys.exit(1)
         return
 
     line = {
@@ -517,27 +657,44 @@ def main():
                      "peak_source": "measured: am_probe_fp64_tflops DFMA microbenchmark on this GPU "
                                     "(MEASURED_PEAKS.json has no fp64 entry)",
                      "work_per_launch": f"{fl:.4g} algorithmic fp64 flops per step (SURVEY §8d: 1072*N_it + 2273 per eval); "
-                                    "one step = the Newton kernel + the tangent kernel"},
+                                        "one step = the Newton kernel + the tangent kernel"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "evaluator.evaluate_arrays (the reference's drop-in call) with the caller's pageable numpy "
+                        "arrays -> am_eval_batch_host: pinned staging of the inputs by a host copy pool, results "
+                        "returned in pooled page-locked numpy arrays, 3-stream chunked H2D|kernels|D2H",
+                "c_abi_pinned": {"value": abi_value, "unit": UNIT,
+                                 "path": "am_eval_batch_host (C ABI) with caller-pinned host AoS buffers"},
                 "pcie_ceiling": pcie_ceiling, "frac_of_pcie_ceiling": e2e_value / world / pcie_ceiling,
-                "pcie_ceiling_note": "same bytes as concurrent pinned H2D + D2H copies without kernels (per GPU)",
-                "path": "am_eval_batch_host (C ABI), pinned host AoS buffers, 3-stream chunked (ramp 2^12 .. 2^17 points) H2D|kernels|D2H"},
+                "pcie_ceiling_note": "same bytes as concurrent pinned H2D + D2H copies without kernels (per GPU)"},
         "gpu_launches": 2 * args.steps,
+        "gpu_launches_note": "K1 launches (Newton + tangent kernel) of the config-2 timed region",
         "clocks": clocks,
+        "basic_scheme": basic,
     }
-    line["strategies"] = strategies
-    line["strategies_note"] = ("config-2 batch, stress + tangent, device-resident, 5 launches each after 2 warm-up; "
-                               "conventional = the paper's hand-derived radial return baseline")
-    if path is not None:
-        line["loading_path"] = path
-    if basic is not None:
-        line["basic_scheme"] = basic
-        line["gpu_launches_note"] = "gpu_launches counts the config-2 K1 launches of the timed region"
+    if strategies:
+        line["strategies"] = strategies
+        line["strategies_note"] = ("config-2 batch, stress + tangent, device-resident, 5 launches each after 2 "
+                                   "warm-up; conventional = the paper's hand-derived radial return baseline")
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
+        if args.basic or args.path:
+            threads = os.cpu_count() or 1
+            s64 = oracle_basic_seconds_per_iteration(64)
+            ref = {"seconds_per_iteration_64": s64, "cores": threads, "kind": "port",
+                   "sample": "2 iterations of load step 1 at 64^3 (C restatement of the automatic route, all host "
+                             "threads, + numpy field step), N-scaled to the config's grid"}
+            for key, n in (("config4_step1", args.basic), ("config3_path", args.path)):
+                if n and key in basic and "error" not in basic[key]:
+                    s = s64 * (n / 64) ** 3
+                    basic[key]["cpu_baseline"] = dict(ref, value=1.0 / s, unit="it/s",
+                                                      seconds_per_iteration_scaled=s)
+    if errors:
+        line["error"] = f"basic-scheme runs failed: {', '.join(errors)}"
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+    if errors:
+        sys.exit(1)
 
 
 if __name__ == "__main__":

@@ -93,6 +93,13 @@ const char *am_version(void);
 int am_device_count(int *count);
 int am_set_device(int device);
 
+/* Page-locked host memory for result arrays (cached pool; no reference
+ * counterpart): the Python shim returns evaluate_arrays' outputs in such
+ * blocks so the D2H copies land in them directly.  am_host_free returns a
+ * block to the pool. */
+int am_host_alloc(int64_t bytes, void **out);
+int am_host_free(void *p);
+
 /* ---------------------------------------------------------------- material points
  * am_eval_batch -- replaces gsmkit.evaluator.evaluate_arrays
  * (evaluator.py:206-248) for the automatic implicit-Euler route.

@@ -95,6 +95,8 @@ SIGNATURES = {
         _dp, _dp, _dp, _dp, ctypes.c_int, _dp, _dp, _dp, _i32p, _i32p, _i64p, _dp, _u8p,
     ]),
     "am_probe_fp64_tflops": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
+    "am_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "am_host_free": (ctypes.c_int, [_vp]),
     "am_lawops_host": (ctypes.c_int, [
         ctypes.POINTER(am_law), ctypes.c_int, ctypes.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
     ]),
@@ -262,3 +264,32 @@ def f64(a, shape=None):
     if shape is not None:
         a = a.reshape(shape)
     return a
+
+
+class _PinnedBlock:
+    """A page-locked host block from the library's pool (am_host_alloc),
+    returned to the pool when the last array viewing it is released."""
+
+    __slots__ = ("ptr",)
+
+    def __init__(self, nbytes):
+        p = ctypes.c_void_p()
+        check(load().am_host_alloc(int(nbytes), ctypes.byref(p)), "pinned host allocation")
+        self.ptr = p.value
+
+    def __del__(self):
+        if self.ptr and _LIB is not None:
+            _LIB.am_host_free(ctypes.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def pinned_empty(shape, dtype=np.float64):
+    """Uninitialised numpy array in page-locked host memory (result arrays of
+    the host entry points: the device copies land in them directly)."""
+    dtype = np.dtype(dtype)
+    count = int(np.prod(shape))
+    nbytes = max(count * dtype.itemsize, 1)
+    blk = _PinnedBlock(nbytes)
+    buf = (ctypes.c_char * nbytes).from_address(blk.ptr)
+    buf._block = blk  # the block lives as long as any view of buf
+    return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)

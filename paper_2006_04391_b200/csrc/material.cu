@@ -12,7 +12,12 @@
 // (coalesced: consecutive threads touch consecutive doubles) and the
 // reference's AoS host layout on the host-pointer path.
 #include <algorithm>
+#include <condition_variable>
+#include <emmintrin.h>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "k1_kernels.cuh"
@@ -221,13 +226,119 @@ extern "C" int am_eval_batch(const am_law* law, const am_cfg* cfg, int64_t B, co
 
 namespace {
 
+// Parallel host memcpy for the staging of pageable host arrays: a small
+// persistent pool; run() splits the copies into 1 MiB segments that the
+// workers and the caller take in order and returns when all are done.
+struct CopyPool {
+    struct Seg {
+        char* d;
+        const char* s;
+        size_t n;
+    };
+    std::vector<std::thread> workers;
+    std::mutex mu;
+    std::condition_variable cv_work, cv_done;
+    std::vector<Seg> jobs;
+    size_t idx = 0, remaining = 0;
+    bool stop = false;
+
+    void ensure() {
+        if (!workers.empty()) return;
+        // measured on the B200 boxes (16 vCPUs, tools/e2e_probe.py): 5 workers + the caller
+        // saturate the host memory bandwidth the copies share with the DMA
+        int n = std::min(5, (int)std::thread::hardware_concurrency() - 1);
+        if (const char* e = std::getenv("AM_COPY_THREADS")) n = std::atoi(e);
+        n = std::max(0, std::min(n, 16));
+        for (int i = 0; i < n; ++i) workers.emplace_back([this] { loop(); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv_work.notify_all();
+        for (auto& t : workers) t.join();
+    }
+    // streaming (non-temporal) stores: the staging buffers are read next by
+    // the DMA engine, not by this CPU, and skipping the read-for-ownership
+    // of the destination saves a sixth of the host memory traffic of the
+    // path (which is host-DRAM bound with pageable inputs)
+    static void copy_nt(char* d, const char* s, size_t n) {
+        size_t head = (16 - ((uintptr_t)d & 15)) & 15;
+        if (head > n) head = n;
+        std::memcpy(d, s, head);
+        d += head, s += head, n -= head;
+        const size_t body = n & ~size_t(63);
+        for (size_t o = 0; o < body; o += 64) {
+            const __m128i a = _mm_loadu_si128((const __m128i*)(s + o));
+            const __m128i b = _mm_loadu_si128((const __m128i*)(s + o + 16));
+            const __m128i c = _mm_loadu_si128((const __m128i*)(s + o + 32));
+            const __m128i e = _mm_loadu_si128((const __m128i*)(s + o + 48));
+            _mm_stream_si128((__m128i*)(d + o), a);
+            _mm_stream_si128((__m128i*)(d + o + 16), b);
+            _mm_stream_si128((__m128i*)(d + o + 32), c);
+            _mm_stream_si128((__m128i*)(d + o + 48), e);
+        }
+        std::memcpy(d + body, s + body, n - body);
+        _mm_sfence();
+    }
+    void drain(std::unique_lock<std::mutex>& lk) {
+        while (idx < jobs.size()) {
+            const Seg g = jobs[idx++];
+            lk.unlock();
+            copy_nt(g.d, g.s, g.n);
+            lk.lock();
+            if (--remaining == 0) cv_done.notify_all();
+        }
+    }
+    void loop() {
+        std::unique_lock<std::mutex> lk(mu);
+        for (;;) {
+            cv_work.wait(lk, [&] { return stop || idx < jobs.size(); });
+            if (stop) return;
+            drain(lk);
+        }
+    }
+    static void add(std::vector<Seg>& v, void* d, const void* s, size_t n) {
+        constexpr size_t kSeg = size_t(1) << 20;
+        for (size_t o = 0; o < n; o += kSeg) v.push_back({(char*)d + o, (const char*)s + o, std::min(kSeg, n - o)});
+    }
+    void run(std::vector<Seg>& segs) {
+        if (segs.empty()) return;
+        ensure();
+        std::unique_lock<std::mutex> lk(mu);
+        jobs.swap(segs);
+        idx = 0;
+        remaining = jobs.size();
+        cv_work.notify_all();
+        drain(lk);
+        cv_done.wait(lk, [&] { return remaining == 0; });
+        jobs.clear();
+        segs.clear();
+        idx = 0;
+    }
+};
+
+bool host_pinned(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
 // Device staging for the host-pointer path: chunks of 2^17 points cycle
 // through three slots / streams so that the H2D copy of one chunk, the
 // kernels of another and the D2H copy of a third overlap (the paper's
 // two-stream staging, with device-resident buffers reused
 // across calls).  The path is PCIe-bound by the D2H of C (288 B/point);
 // 3 x 2^17 measured best (tools/e2e_variants.py: 8.67 ms per 2^20 vs
-// 9.0-9.2 ms for 2 x 2^18).
+// 9.0-9.2 ms for 2 x 2^18).  Pageable (unregistered) host arrays go through
+// pinned per-slot staging buffers, filled / drained by the CopyPool while
+// the other slots' DMA runs (a pageable cudaMemcpyAsync would stage
+// synchronously and serialise the pipeline).
 struct HostPipe {
 #ifndef AM_HOST_SLOTS
 #define AM_HOST_SLOTS 3
@@ -239,12 +350,19 @@ struct HostPipe {
     int device = -1;
     int64_t cap = 0;
     cudaStream_t stream[kSlots] = {};
+    cudaEvent_t done[kSlots] = {};
     double* in[kSlots] = {};     // eps_n | a_n | eps_np1 | dt
     double* out[kSlots] = {};    // sigma | a_out | C
     int32_t* iters[kSlots] = {};
     uint8_t* status[kSlots] = {};
+    char* hin[kSlots] = {};      // pinned staging: inputs (20 doubles / point)
+    char* hout[kSlots] = {};     // pinned staging: outputs (49 doubles + 2 int32 + 1 byte / point)
     uint32_t* flags = nullptr;   // kSlots words
+    CopyPool pool;
     std::mutex mu;
+
+    static constexpr size_t kInBytes = 20 * sizeof(double);
+    static constexpr size_t kOutBytes = 49 * sizeof(double) + 2 * sizeof(int32_t) + 1;
 
     int ensure(int64_t chunk) {
         int dev;
@@ -254,6 +372,7 @@ struct HostPipe {
         device = dev;
         for (int s = 0; s < kSlots; ++s) {
             AM_CUDA(cudaStreamCreateWithFlags(&stream[s], cudaStreamNonBlocking));
+            AM_CUDA(cudaEventCreateWithFlags(&done[s], cudaEventDisableTiming));
             AM_CUDA(cudaMalloc(&in[s], sizeof(double) * chunk * 20));
             AM_CUDA(cudaMalloc(&out[s], sizeof(double) * chunk * 49));
             AM_CUDA(cudaMalloc(&iters[s], sizeof(int32_t) * 2 * chunk));  // iters | rejected
@@ -263,12 +382,22 @@ struct HostPipe {
         cap = chunk;
         return AM_OK;
     }
+    int ensure_staging() {
+        for (int s = 0; s < kSlots; ++s) {
+            if (!hin[s]) AM_CUDA(cudaHostAlloc((void**)&hin[s], kInBytes * cap, cudaHostAllocPortable));
+            if (!hout[s]) AM_CUDA(cudaHostAlloc((void**)&hout[s], kOutBytes * cap, cudaHostAllocPortable));
+        }
+        return AM_OK;
+    }
     void release() {
         if (device < 0) return;
         for (int s = 0; s < kSlots; ++s) {
             cudaFree(in[s]); cudaFree(out[s]); cudaFree(iters[s]); cudaFree(status[s]);
+            cudaFreeHost(hin[s]); cudaFreeHost(hout[s]);
             if (stream[s]) cudaStreamDestroy(stream[s]);
+            if (done[s]) cudaEventDestroy(done[s]);
             in[s] = out[s] = nullptr; iters[s] = nullptr; status[s] = nullptr; stream[s] = nullptr;
+            hin[s] = hout[s] = nullptr; done[s] = nullptr;
         }
         cudaFree(flags);
         flags = nullptr;
@@ -299,50 +428,105 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
     std::lock_guard<std::mutex> lock(P.mu);
     const int64_t chunk = B < (int64_t(1) << AM_HOST_CHUNK_LOG2) ? B : (int64_t(1) << AM_HOST_CHUNK_LOG2);
     AM_TRY(P.ensure(chunk));
+    // which host arrays need staging (pageable memory)
+    const double* ins[4] = {eps_n, m ? a_n : nullptr, eps_np1, dt};
+    const int inw[4] = {6, m, 6, 1};                         // doubles per point
+    void* outs[6] = {sigma, m ? a_out : nullptr, want_tangent ? C : nullptr, newton_iters, rejected, status};
+    const int outb[6] = {6 * 8, m * 8, 36 * 8, 4, 4, 1};     // bytes per point
+    bool stage_in[4], stage_out[6], any_stage = false;
+    for (int i = 0; i < 4; ++i) any_stage |= (stage_in[i] = ins[i] && !host_pinned(ins[i]));
+    for (int i = 0; i < 6; ++i) any_stage |= (stage_out[i] = outs[i] && !host_pinned(outs[i]));
+    if (any_stage) AM_TRY(P.ensure_staging());
     AM_CUDA(cudaMemsetAsync(P.flags, 0, sizeof(uint32_t) * HostPipe::kSlots, P.stream[0]));
     AM_CUDA(cudaStreamSynchronize(P.stream[0]));
+    std::vector<CopyPool::Seg> segs;
+    int64_t plo[HostPipe::kSlots], pn[HostPipe::kSlots];
+    bool live[HostPipe::kSlots] = {};
+    // staged outputs of the chunk in slot s -> the caller's arrays
+    auto drain = [&](int s) -> int {
+        if (!live[s]) return AM_OK;
+        AM_CUDA(cudaEventSynchronize(P.done[s]));
+        size_t off = 0;
+        for (int i = 0; i < 6; ++i) {
+            if (!outs[i]) continue;
+            const size_t nb = (size_t)outb[i] * pn[s];
+            if (stage_out[i]) CopyPool::add(segs, (char*)outs[i] + (size_t)outb[i] * plo[s], P.hout[s] + off, nb);
+            off += nb;
+        }
+        P.pool.run(segs);
+        live[s] = false;
+        return AM_OK;
+    };
     // chunk sizes ramp up from 2^AM_HOST_RAMP_LOG2 so the first D2H starts
     // early (pipeline fill), then stay at `chunk`
 #ifndef AM_HOST_RAMP_LOG2
 #define AM_HOST_RAMP_LOG2 12
 #endif
-    int64_t lo = 0;
-    for (int64_t c = 0; lo < B; ++c) {
+    int64_t lo = 0, c = 0;
+    for (; lo < B; ++c) {
         const int s = int(c % HostPipe::kSlots);
         cudaStream_t st = P.stream[s];
+        AM_TRY(drain(s));  // the slot's previous chunk is complete
         int64_t want = chunk;
         if (AM_HOST_RAMP_LOG2 + c < AM_HOST_CHUNK_LOG2) want = int64_t(1) << (AM_HOST_RAMP_LOG2 + c);
         const int64_t n = (B - lo) < want ? (B - lo) : want;
-        double* d_en = P.in[s];
-        double* d_an = d_en + 6 * n;
-        double* d_e1 = d_an + 7 * n;
-        double* d_dt = d_e1 + 6 * n;
+        double* d_in[4];
+        d_in[0] = P.in[s];
+        d_in[1] = d_in[0] + 6 * n;
+        d_in[2] = d_in[1] + 7 * n;
+        d_in[3] = d_in[2] + 6 * n;
+        // inputs: stage the pageable ones, then H2D
+        {
+            size_t off = 0;
+            const char* src[4];
+            for (int i = 0; i < 4; ++i) {
+                if (!ins[i]) continue;
+                const size_t nb = sizeof(double) * inw[i] * n;
+                const char* user = (const char*)(ins[i] + (size_t)inw[i] * lo);
+                if (stage_in[i]) {
+                    CopyPool::add(segs, P.hin[s] + off, user, nb);
+                    src[i] = P.hin[s] + off;
+                    off += nb;
+                } else {
+                    src[i] = user;
+                }
+            }
+            P.pool.run(segs);
+            for (int i = 0; i < 4; ++i)
+                if (ins[i])
+                    AM_CUDA(cudaMemcpyAsync(d_in[i], src[i], sizeof(double) * inw[i] * n, cudaMemcpyHostToDevice, st));
+        }
         double* d_sig = P.out[s];
         double* d_ao = d_sig + 6 * n;
         double* d_C = d_ao + 7 * n;
-        AM_CUDA(cudaMemcpyAsync(d_en, eps_n + 6 * lo, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, st));
-        if (m) AM_CUDA(cudaMemcpyAsync(d_an, a_n + m * lo, sizeof(double) * m * n, cudaMemcpyHostToDevice, st));
-        AM_CUDA(cudaMemcpyAsync(d_e1, eps_np1 + 6 * lo, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, st));
-        AM_CUDA(cudaMemcpyAsync(d_dt, dt + lo, sizeof(double) * n, cudaMemcpyHostToDevice, st));
         KArgs k{};
         k.B = n; k.gidx = nullptr;
-        k.eps_n = d_en; k.a_n = d_an; k.eps_np1 = d_e1; k.dt = d_dt; k.dt_scalar = 0.0;
+        k.eps_n = d_in[0]; k.a_n = d_in[1]; k.eps_np1 = d_in[2]; k.dt = d_in[3]; k.dt_scalar = 0.0;
         k.le = {1, 6}; k.la = {1, m}; k.lc = {1, 36};
         k.sigma = d_sig; k.a_out = d_ao; k.C = want_tangent ? d_C : nullptr;
         k.iters = P.iters[s]; k.rejected = P.iters[s] + n; k.status = P.status[s]; k.flags = P.flags + s;
         set_controls(k, cfg);
         AM_TRY(launch_material(law, k, st));
-        AM_CUDA(cudaMemcpyAsync(sigma + 6 * lo, d_sig, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, st));
-        if (m) AM_CUDA(cudaMemcpyAsync(a_out + m * lo, d_ao, sizeof(double) * m * n, cudaMemcpyDeviceToHost, st));
-        if (want_tangent)
-            AM_CUDA(cudaMemcpyAsync(C + 36 * lo, d_C, sizeof(double) * 36 * n, cudaMemcpyDeviceToHost, st));
-        if (newton_iters)
-            AM_CUDA(cudaMemcpyAsync(newton_iters + lo, P.iters[s], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
-        if (rejected)
-            AM_CUDA(cudaMemcpyAsync(rejected + lo, P.iters[s] + n, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
-        if (status) AM_CUDA(cudaMemcpyAsync(status + lo, P.status[s], n, cudaMemcpyDeviceToHost, st));
+        // outputs: D2H straight into pinned caller arrays, else into the slot's staging
+        {
+            const void* dsrc[6] = {d_sig, d_ao, d_C, P.iters[s], P.iters[s] + n, P.status[s]};
+            size_t off = 0;
+            for (int i = 0; i < 6; ++i) {
+                if (!outs[i]) continue;
+                const size_t nb = (size_t)outb[i] * n;
+                void* dst = stage_out[i] ? (void*)(P.hout[s] + off) : (void*)((char*)outs[i] + (size_t)outb[i] * lo);
+                AM_CUDA(cudaMemcpyAsync(dst, dsrc[i], nb, cudaMemcpyDeviceToHost, st));
+                off += nb;
+            }
+        }
+        AM_CUDA(cudaEventRecord(P.done[s], st));
+        plo[s] = lo;
+        pn[s] = n;
+        live[s] = true;
         lo += n;
     }
+    // drain the remaining slots in chunk order
+    for (int64_t j = c; j < c + HostPipe::kSlots; ++j) AM_TRY(drain(int(j % HostPipe::kSlots)));
     uint32_t flags[HostPipe::kSlots];
     AM_CUDA(cudaMemcpyAsync(flags, P.flags, sizeof(flags), cudaMemcpyDeviceToHost, P.stream[0]));
     for (int s = 0; s < HostPipe::kSlots; ++s) AM_CUDA(cudaStreamSynchronize(P.stream[s]));

@@ -203,3 +203,66 @@ def test_evaluate_batch_groups_and_config_errors(api):
     for i in (1, 2, 4, 5):
         one = evaluate(gsm.MichelSuquet(), cfg, reqs[i])
         assert np.array_equal(res[i].sigma, one.sigma) and np.array_equal(res[i].C, one.C)
+
+
+def test_host_entry_pageable_vs_pinned(api):
+    """am_eval_batch_host stages pageable arrays through pinned slots (3-slot
+    pipeline, chunk ramp 2^12 .. 2^17): results equal the pinned-array path
+    bit for bit, for a batch spanning many chunks, every output array
+    pageable or pinned in any mix."""
+    import torch
+
+    gsm, cfg, ev = api
+    from paper_2006_04391_b200 import _lib
+    from paper_2006_04391_b200.workloads import config2_batch
+
+    B = 300_001
+    en, an, ep, dt = config2_batch(B, seed=17)
+    lib = _lib.load()
+    law, c = _lib.make_law(gsm.MichelSuquet()), _lib.make_cfg(cfg)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+
+    def run(inputs, pinned_out):
+        alloc = (lambda s, d=np.float64: torch.empty(s, dtype=getattr(torch, np.dtype(d).name)).pin_memory().numpy()) \
+            if pinned_out else (lambda s, d=np.float64: np.full(s, 7, dtype=d))
+        sig, a, C = alloc((B, 6)), alloc((B, 7)), alloc((B, 6, 6))
+        it, st = alloc((B,), np.int32), alloc((B,), np.uint8)
+        _lib.check(lib.am_eval_batch_host(law, c, B, *[_lib.ptr(x) for x in inputs], 1, _lib.ptr(sig), _lib.ptr(a),
+                                          _lib.ptr(C), _lib.ptr(it, _lib._i32p), None, _lib.ptr(st, _lib._u8p)))
+        return sig, a, C, it, st
+
+    pageable = (en, an, ep, dt)
+    pinned = tuple(pin(x) for x in pageable)
+    mixed = (en, pinned[1], ep, pinned[3])
+    base = run(pinned, True)
+    for inputs, po in ((pageable, False), (pageable, True), (pinned, False), (mixed, False)):
+        got = run(inputs, po)
+        for x, y in zip(got, base):
+            assert np.array_equal(x, y)
+    assert np.all(base[4] == 0)
+
+
+def test_evaluate_arrays_results_from_pool(api):
+    """evaluate_arrays returns its results in recycled page-locked blocks:
+    every element is rewritten (garbage planted in the pool never shows)."""
+    gsm, cfg, ev = api
+    from paper_2006_04391_b200 import _lib
+    from paper_2006_04391_b200.workloads import config2_batch
+
+    B = 50_000
+    en, an, ep, dt = config2_batch(B, seed=3)
+    ref = ev(gsm.MichelSuquet(), cfg, en, an, ep, dt, want_tangent=True)
+    ref = (ref.sigma.copy(), ref.a.copy(), ref.C.copy(), ref.newton_iters.copy())
+    for law, m in ((gsm.MichelSuquet(), 7), (gsm.LinearElastic(300e9, 0.25), 0)):
+        junk = [_lib.pinned_empty(s) for s in ((B, 6), (B, 7), (B, 6, 6), (B, 2))]
+        for j in junk:
+            j.fill(np.nan)
+        del junk, j  # back to the pool
+        r = ev(law, cfg, en, an[:, :m], ep, dt, want_tangent=True)
+        assert np.all(np.isfinite(r.sigma)) and np.all(np.isfinite(r.C)) and np.all(np.isfinite(r.a))
+        assert np.all(r.substeps == 1) and np.all(r.rejected == 0)
+        if m:
+            assert np.array_equal(r.sigma, ref[0]) and np.array_equal(r.C, ref[2])
+            assert np.array_equal(r.newton_iters, ref[3])
+        else:
+            assert np.all(r.newton_iters == 0)
