@@ -756,8 +756,8 @@ static int fourier_pass_x(am_solver* h, std::vector<double>& out) {
     const int64_t tiles = (ncol + kXJ - 1) / kXJ;
     int sms = 148;
     AM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-    k_xfourier<<<(unsigned)(kXNB == 2 ? std::min<int64_t>(tiles, sms) : tiles), kXThreads, kXSmem, h->stream>>>(h->nx, h->ny, h->nz, s.sp.cs, ref, s.S, s.ehat, h->red,
-                                                         h->redP);
+    k_xfourier<<<(unsigned)std::min<int64_t>(tiles, (int64_t)sms * kXCtas), kXThreads, kXSmem, h->stream>>>(
+        h->nx, h->ny, h->nz, s.sp.cs, ref, s.S, s.ehat, h->red, h->redP);
     AM_CUDA(cudaGetLastError());
     out.resize(L);
     return reduce_to_host(h, out.data());

@@ -16,17 +16,23 @@
 // k_origin_x, once the host has solved the mixed boundary conditions
 // (its inverse x transform is the constant ebar along the (ky, kz) = 0 line).
 //
-// CTA tile: XJ consecutive (ky, kz) columns j = ky * nzh + kz (contiguous
-// in memory for each (c, x)), all 256 x and 6 components, staged in shared
-// memory; each of the 6 * XJ lines is transformed by 16 threads with a
-// 16 x 16 decomposition (radix-16 DFTs in registers, one table of 256
-// twiddles, lines padded to 17-element rows against bank conflicts).
+// CTA tile (v3): XJ = 2 consecutive (ky, kz) columns j = ky * nzh + kz (a
+// 32-byte sector for each (c, x)), all 256 x and 6 components, staged in
+// shared memory (52 KB: 4 CTAs per SM, a persistent grid).  Each of the 12
+// lines is transformed by 16 threads of one warp with a 16 x 16
+// decomposition (radix-16 DFTs in registers, one table of 256 twiddles,
+// lines padded to 17-element rows against bank conflicts) and only warp
+// barriers; CTA barriers separate load / Fourier update / store.  v2 (4
+// columns, 384 threads, CTA-wide barriers inside the FFTs, 1 CTA per SM)
+// was issue-latency bound at 12 warps per SM (1.44 ms at 256^3).
 // Residual partials are per tile, reduced in a fixed order.
 //
-// Status: opt-in (AM_XFUSED=1).  Parity-tested, but at 256^3 the kernel is
-// issue-latency bound (1.44 ms vs 0.62 ms k_fourier + 2 x 0.27 ms cuFFT x
-// passes; the 2-D plans save 0.55 ms): net 2.80 vs 2.53 ms per iteration
-// (profiles/r01/k1_variants.log, r26).
+// Status: opt-in (AM_XFUSED=1).  Parity-tested; at 256^3 v3 takes 1.30 ms
+// (2 CTAs/SM, no spills; 1.38 at 3, 1.93 at 4 with spills) against 1.16 ms
+// for k_fourier + cuFFT's two x passes, so the 3-D cuFFT path stays the
+// default: the 32-byte (c, x) rows of a 2-column tile give the DRAM poor
+// locality, and tiles wide enough for 128-byte rows need ~200 KB of shared
+// memory (profiles/r01/k1_variants.log, r2 entries).
 #pragma once
 
 #include "fourier.cuh"
@@ -34,15 +40,15 @@
 namespace am {
 
 constexpr int kXN = 256;                 // supported nx
-constexpr int kXJ = 4;                   // (ky, kz) columns per CTA
-constexpr int kXLines = 6 * kXJ;         // lines per CTA
-constexpr int kXThreads = kXLines * 16;  // 16 threads per line
-#ifndef AM_XF_NB
-#define AM_XF_NB 2
+constexpr int kXJ = 2;                   // (ky, kz) columns per tile
+constexpr int kXLines = 6 * kXJ;         // lines per tile
+constexpr int kXThreads = kXLines * 16;  // 16 threads per line: 192
+#ifndef AM_XF_CTAS
+#define AM_XF_CTAS 2
 #endif
-constexpr int kXNB = AM_XF_NB;           // tile buffers: 2 = persistent with prefetch, 1 = a tile per CTA
+constexpr int kXCtas = AM_XF_CTAS;       // resident CTAs per SM
 constexpr int kXRow = 273;               // padded line: pos(x) = (x & 15) + 17 (x >> 4) < 271;
-                                         // odd, so the XJ columns of a component sit in different banks
+                                         // odd, so the two columns of a component sit in different banks
 
 __device__ __forceinline__ int xpos(int x) { return (x & 15) + 17 * (x >> 4); }
 
@@ -107,8 +113,9 @@ __device__ __forceinline__ void dft16(double2* v) {
     t = v[11]; v[11] = v[14]; v[14] = t;
 }
 
-// 256-point DFT (sign S) of every line of buf, natural order at xpos();
-// thread i of its line.  tw[m] = exp(-2 pi i m / 256).
+// 256-point DFT (sign S) of one line, natural order at xpos(); thread i
+// (0..15) of the 16 threads of its line, which share a warp (warp barriers
+// only).  tw[m] = exp(-2 pi i m / 256).
 template <int S>
 __device__ __forceinline__ void line_fft256(double2* line, const double2* tw, int i) {
     double2 v[16];
@@ -121,104 +128,71 @@ __device__ __forceinline__ void line_fft256(double2* line, const double2* tw, in
         const double2 w = tw[i * k1];
         v[k1] = cmul(v[k1], make_double2(w.x, S < 0 ? w.y : -w.y));
     }
+    __syncwarp();
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) line[i + 17 * k1] = v[k1];
-    __syncthreads();
+    __syncwarp();
     // k1 = i: DFT16 over n1 -> X[k1 + 16 k2]
 #pragma unroll
     for (int n1 = 0; n1 < 16; ++n1) v[n1] = line[n1 + 17 * i];
     dft16<S>(v);
-    __syncthreads();
+    __syncwarp();
 #pragma unroll
     for (int k2 = 0; k2 < 16; ++k2) line[i + 17 * k2] = v[k2];
-    __syncthreads();
+    __syncwarp();
 }
 
-// 16-byte asynchronous global -> shared copy; zero fill when !valid
-__device__ __forceinline__ void cp_async16(double2* dst, const double2* src, bool valid) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-// stage tile `tile` of the 2-D spectra into buf (asynchronous)
-__device__ __forceinline__ void xtile_load(double2* buf, const double2* __restrict__ S, int64_t cs, int64_t ncol,
-                                           int64_t tile) {
-    const int64_t j0 = tile * kXJ;
-#pragma unroll
-    for (int r = 0; r < 6 * kXN * kXJ / kXThreads; ++r) {
-        const int e = threadIdx.x + r * kXThreads;
-        const int jj = e & (kXJ - 1), x = (e / kXJ) & (kXN - 1), c = e / (kXJ * kXN);
-        const int64_t j = j0 + jj;
-        cp_async16(buf + (c * kXJ + jj) * kXRow + xpos(x), S + (j < ncol ? c * cs + x * ncol + j : 0), j < ncol);
-    }
-}
-
-// Persistent: CTA b handles tiles b, b + grid, ... with the next tile's
-// spectra prefetched (cp.async) into the second buffer while the current one
-// is transformed and updated.  red[tile] = the tile's residual partial;
-// red[P + c] = Re sigma_hat(origin) (the caller zeroes the slots).
-__global__ void __launch_bounds__(kXThreads, kXNB == 1 ? 2 : 1) k_xfourier(int nx, int ny, int nz, int64_t cs, RefMat ref,
-                                                           double2* __restrict__ S, double2* __restrict__ ehat,
-                                                           double* __restrict__ red, int64_t P) {
+// Persistent: CTA b handles tiles b, b + grid, ...  red[tile] = the tile's
+// residual partial; red[P + c] = Re sigma_hat(origin) (the caller zeroes the
+// slots).  S: 2-D spectra (c, x, j) in, 2-D spectra of the next eps (without
+// its origin, k_origin_x) out; ehat: rfft(eps) (c, kx, j) in / out.
+__global__ void __launch_bounds__(kXThreads, kXCtas) k_xfourier(int nx, int ny, int nz, int64_t cs, RefMat ref,
+                                                                double2* __restrict__ S, double2* __restrict__ ehat,
+                                                                double* __restrict__ red, int64_t P) {
     extern __shared__ double2 xsm[];
-    double2* tw = xsm + kXNB * kXLines * kXRow;  // [256]
+    double2* tw = xsm + kXLines * kXRow;  // [256]
     __shared__ double rsh[kXThreads / 32];
     const int nzh = nz / 2 + 1;
-    const int64_t ncol = (int64_t)ny * nzh;  // = xs
+    const int64_t ncol = (int64_t)ny * nzh;  // = x stride of the 2-D spectra
     const int64_t ntiles = (ncol + kXJ - 1) / kXJ;
     const int t = threadIdx.x;
-    if (t < kXN) {
+    for (int m = t; m < kXN; m += kXThreads) {
         double s, c;
-        sincospi(-(double)t / 128.0, &s, &c);
-        tw[t] = make_double2(c, s);
+        sincospi(-(double)m / 128.0, &s, &c);
+        tw[m] = make_double2(c, s);
     }
-    const int L = t >> 4, i = t & 15;
+    const int L = t >> 4, i = t & 15;  // line L = c * kXJ + jj
+    double2* line = xsm + L * kXRow;
     const double invN = 1.0 / ((double)nx * ny * nz);
-    int cur = 0;
-    if (blockIdx.x < ntiles) xtile_load(xsm, S, cs, ncol, blockIdx.x);
-    cp_async_commit();
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, cur ^= 1) {
-        double2* buf = xsm + (kXNB == 2 ? cur : 0) * kXLines * kXRow;
-        if (kXNB == 1 && tile != blockIdx.x) xtile_load(buf, S, cs, ncol, tile);
-        if (kXNB == 2 && tile + gridDim.x < ntiles)
-            xtile_load(xsm + (cur ^ 1) * kXLines * kXRow, S, cs, ncol, tile + gridDim.x);
-        cp_async_commit();
-        // ehat of this thread's bins of the tile in flight during the forward transform
+    constexpr int kE = kXLines * kXN / kXThreads;  // tile elements per thread: 16
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t j0 = tile * kXJ;
-        constexpr int kB = (kXN * kXJ + kXThreads - 1) / kXThreads;
-        double2 ev[kB][6];
+        // load: element e -> (c, x, jj), consecutive threads take the two
+        // columns of one (c, x) row (a 32-byte sector)
 #pragma unroll
-        for (int r = 0; r < kB; ++r) {
-            const int b = t + r * kXThreads;
-            const int jj = b & (kXJ - 1), kx = b / kXJ;
+        for (int r = 0; r < kE; ++r) {
+            const int e = t + r * kXThreads;
+            const int jj = e & (kXJ - 1), x = (e / kXJ) & (kXN - 1), c = e / (kXJ * kXN);
             const int64_t j = j0 + jj;
-            const bool ok = b < kXN * kXJ && j < ncol;
-#pragma unroll
-            for (int c = 0; c < 6; ++c)
-                ev[r][c] = ok ? ehat[c * cs + (int64_t)kx * ncol + j] : make_double2(0.0, 0.0);
+            xsm[(c * kXJ + jj) * kXRow + xpos(x)] = j < ncol ? __ldg(S + c * cs + x * ncol + j) : make_double2(0.0, 0.0);
         }
-        cp_async_wait<1>();
         __syncthreads();
-        line_fft256<-1>(buf + L * kXRow, tw, i);
+        line_fft256<-1>(line, tw, i);
+        __syncthreads();
+        // Fourier update of the tile's 2 x 256 bins
         double acc = 0.0;
-#pragma unroll
-        for (int r = 0; r < kB; ++r) {
-            const int b = t + r * kXThreads;
+        for (int b = t; b < kXN * kXJ; b += kXThreads) {
             const int jj = b & (kXJ - 1), kx = b / kXJ;
             const int64_t j = j0 + jj;
-            if (b >= kXN * kXJ || j >= ncol) continue;
-            const int ky = (int)j / nzh, kz = (int)j - ky * nzh;  // ncol < 2^31
+            if (j >= ncol) continue;
+            const int ky = (int)(j / nzh), kz = (int)(j - (int64_t)ky * nzh);
             const Bin bn = make_bin(kx, ky, kz, nx, ny, nz);
-            double2* cell = buf + jj * kXRow + xpos(kx);  // component c at cell[c * kXJ * kXRow]
+            double2* cell = xsm + jj * kXRow + xpos(kx);  // component c at cell[c * kXJ * kXRow]
             cplx s[6];
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
-                const double2 v = cell[c * kXJ * kXRow];
-                s[c] = cplx{v.x, v.y};
+                const double2 w = cell[c * kXJ * kXRow];
+                s[c] = cplx{w.x, w.y};
             }
             if (bn.zero) {
 #pragma unroll
@@ -229,11 +203,13 @@ __global__ void __launch_bounds__(kXThreads, kXNB == 1 ? 2 : 1) k_xfourier(int n
                 continue;
             }
             acc += rfft_weight(kz, nz) * traction_sq(bn, s);
-            double cr[6], ci[6], tr[6], ti[6], outr[6], outi[6], er[6], ei[6];
+            const int64_t q = (int64_t)kx * ncol + j;
+            double er[6], ei[6], cr[6], ci[6], tr[6], ti[6], outr[6], outi[6];
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
-                er[c] = ev[r][c].x;
-                ei[c] = ev[r][c].y;
+                const double2 w = ehat[c * cs + q];
+                er[c] = w.x;
+                ei[c] = w.y;
             }
             iso_apply(ref, er, cr);
             iso_apply(ref, ei, ci);
@@ -244,7 +220,6 @@ __global__ void __launch_bounds__(kXThreads, kXNB == 1 ? 2 : 1) k_xfourier(int n
             }
             green_apply_real(ref, bn, tr, outr);
             green_apply_real(ref, bn, ti, outi);
-            const int64_t q = (int64_t)kx * ncol + j;
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
                 ehat[c * cs + q] = make_double2(outr[c], outi[c]);
@@ -261,19 +236,19 @@ __global__ void __launch_bounds__(kXThreads, kXNB == 1 ? 2 : 1) k_xfourier(int n
             for (int w = 0; w < kXThreads / 32; ++w) sum += rsh[w];
             red[tile] = sum;
         }
-        line_fft256<1>(buf + L * kXRow, tw, i);
+        line_fft256<1>(line, tw, i);
+        __syncthreads();
 #pragma unroll
-        for (int r = 0; r < 6 * kXN * kXJ / kXThreads; ++r) {
+        for (int r = 0; r < kE; ++r) {
             const int e = t + r * kXThreads;
             const int jj = e & (kXJ - 1), x = (e / kXJ) & (kXN - 1), c = e / (kXJ * kXN);
             const int64_t j = j0 + jj;
-            if (j < ncol) S[c * cs + x * ncol + j] = buf[(c * kXJ + jj) * kXRow + xpos(x)];
+            if (j < ncol) S[c * cs + x * ncol + j] = xsm[(c * kXJ + jj) * kXRow + xpos(x)];
         }
-        __syncthreads();  // buf is refilled by the prefetch two tiles on
+        __syncthreads();  // the lines are read before the next tile overwrites them
     }
-    cp_async_wait<0>();
 }
 
-constexpr size_t kXSmem = sizeof(double2) * (kXNB * kXLines * kXRow + kXN);
+constexpr size_t kXSmem = sizeof(double2) * (kXLines * kXRow + kXN);
 
 }  // namespace am
