@@ -460,4 +460,215 @@ AM_HD int adaptive_point(const Law& L, const StepCtl& ctl, const double* eps_n, 
     }
 }
 
+#ifdef __CUDACC__
+// ---------------------------------------------------------------- lane groups
+// Coupled integration with the sensitivity split over a group of 6 lanes:
+// lane j advances column j of da/deps_{n+1} (one forward direction: eps_i
+// seeded r [i == j], the state with da[:, j]); the primal state, slopes and
+// step control are computed identically by every lane of the group.  Per
+// direction the arithmetic is the 6-direction sweep's (a dual direction is
+// computed independently of the others), so the results are those of
+// adaptive_point<Law, Scheme, true>; the per-thread live set drops from
+// ~440 doubles (local memory, 116 KB of DRAM traffic per point) to ~120.
+// The error norm gathers the column terms with shuffles and sums them in
+// the reference's (i, j) order (odeint.py:564-617).
+
+template <int... I>
+AM_HD auto eps_lane_tup(const double* e, double r, int j, std::integer_sequence<int, I...>) {
+    auto mk = [&](int i) {
+        D<1u> p;
+        p.v = e[i];
+        p.d[0] = i == j ? r : 0.0;
+        return p;
+    };
+    return tup(mk(I)...);
+}
+template <int... I>
+AM_HD auto a_lane_tup(const double* a, const double* acol, std::integer_sequence<int, I...>) {
+    auto mk = [&](int k) {
+        D<1u> p;
+        p.v = a[k];
+        p.d[0] = acol[k];
+        return p;
+    };
+    return tup(mk(I)...);
+}
+
+// rhs_dual (odeint.py:298-304) for direction j: f and column j of the sensitivity rhs
+template <class Law>
+__device__ __forceinline__ void rhs_dual_lane(const Law& L, const double* e, double r, int j, const double* a,
+                                              const double* acol, double* f, double* fcol) {
+    auto fv = rhs_sweep(L, eps_lane_tup(e, r, j, seq<6>{}), a_lane_tup(a, acol, seq<Law::m>{}));
+    sfor<Law::m>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        f[i] = get<i>(fv).v;
+        fcol[i] = get<i>(fv).template dir<0>();
+    });
+}
+
+// stress_dual (odeint.py:339-352) / stress_tangent column j; acol = nullptr: frozen state
+template <class Law>
+__device__ __forceinline__ void stress_dual_lane(const Law& L, const double* e, double r, int j, const double* a,
+                                                 const double* acol, double* sig, double* ccol) {
+    auto run = [&](const auto& pa) {
+        auto sv = stress_sweep(L, eps_lane_tup(e, r, j, seq<6>{}), pa);
+        sfor<6>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            sig[i] = get<i>(sv).v;
+            ccol[i] = get<i>(sv).template dir<0>();
+        });
+    };
+    if (acol) run(a_lane_tup(a, acol, seq<Law::m>{}));
+    else run(plain_tup<Law::m>(a, seq<Law::m>{}));
+}
+
+// sum over (i, jj) in the reference's order of the group's per-column terms t[i]
+template <int N>
+__device__ __forceinline__ double group_sum(const double* t, unsigned gmask, int gbase) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 6; ++jj) s += __shfl_sync(gmask, t[i], gbase + jj);
+    return s;
+}
+
+// adaptive_point<Law, Scheme, true> by a lane group: every lane returns the
+// same status / counts / primal state a; dacol = column j of da.
+template <class Law, int Scheme>
+__device__ int adaptive_point_lanes(const Law& L, const StepCtl& ctl, const double* eps_n, const double* a_n,
+                                    const double* eps_np1, double dt, double* a, double* dacol, int& substeps,
+                                    int& rejected, int j, unsigned gmask, int gbase, double* rec_h,
+                                    uint8_t* rec_acc) {
+    using T = Tableau<Scheme>;
+    constexpr int m = Law::m;
+    constexpr int s = T::s;
+    for (int i = 0; i < m; ++i) {
+        a[i] = a_n[i];
+        dacol[i] = 0.0;
+    }
+    substeps = rejected = 0;
+    double t = 0.0, h = dt;
+    bool accepted_any = false, g1_valid = false;
+    double g1[m], gd1[m];
+    const int max_attempts = ctl.max_substeps * 4;
+    for (int attempts = 1;; ++attempts) {
+        if (attempts > max_attempts) return ST_INTEGRATION;  // global attempt cap
+        double hi = fmin(h, dt - t);
+        const bool clipped = hi >= dt - t - 1e-15 * dt;
+        double G[s][m], Gd[s][m];
+        double yh[m], yl[m], dh[m], dl[m];
+        bool ok = true;
+        auto stage = [&](int st) {
+            if (st == 0 && g1_valid) {  // FSAL reuse (odeint.py:443-453)
+                for (int i = 0; i < m; ++i) {
+                    G[0][i] = g1[i];
+                    Gd[0][i] = gd1[i];
+                }
+                return;
+            }
+            double yi[m], ydi[m];
+            for (int i = 0; i < m; ++i) {
+                yi[i] = a[i];
+                ydi[i] = dacol[i];
+            }
+            for (int q = 0; q < st; ++q) {
+                const double aq = T::a(st, q);
+                if (aq == 0.0) continue;
+                const double w = hi * aq;
+                for (int i = 0; i < m; ++i) {
+                    yi[i] += w * G[q][i];
+                    ydi[i] += w * Gd[q][i];
+                }
+            }
+            const double ti = t + T::c(st) * hi;
+            double e[6];
+            const double r = strain_at(eps_n, eps_np1, ti, dt, e);
+            rhs_dual_lane(L, e, r, j, yi, ydi, G[st], Gd[st]);
+        };
+        if constexpr (s == 2) {
+            stage(0);
+            stage(1);
+        } else {
+            for (int st = 0; st < s; ++st) stage(st);
+        }
+        for (int i = 0; i < m; ++i) {
+            double sh = 0.0, sl = 0.0, ch = 0.0, cl = 0.0;
+            for (int q = 0; q < s; ++q) {
+                sh += T::b(q) * G[q][i];
+                sl += T::be(q) * G[q][i];
+                ch += T::b(q) * Gd[q][i];
+                cl += T::be(q) * Gd[q][i];
+            }
+            yh[i] = a[i] + hi * sh;
+            yl[i] = a[i] + hi * sl;
+            ok = ok && (yh[i] - yh[i] == 0.0) && (yl[i] - yl[i] == 0.0);
+            dh[i] = dacol[i] + hi * ch;
+            dl[i] = dacol[i] + hi * cl;
+        }
+        // error_norm (odeint.py:564-617)
+        double total;
+        int count;
+        if (ctl.measure == 0) {
+            double p = 0.0, tt[m];
+            for (int i = 0; i < m; ++i) p += scaled_sq(yh[i] - yl[i], a[i], yh[i], ctl.atol, ctl.rtol);
+            for (int i = 0; i < m; ++i) tt[i] = scaled_sq(dh[i] - dl[i], dacol[i], dh[i], ctl.atol, ctl.rtol);
+            total = p + group_sum<m>(tt, gmask, gbase);
+            count = m + 6 * m;
+        } else {
+            double e0[6], e1[6], s0[6], sh[6], sl[6], c0[6], chh[6], cll[6], tc[6];
+            const double r0 = strain_at(eps_n, eps_np1, t, dt, e0);
+            const double r1 = strain_at(eps_n, eps_np1, t + hi, dt, e1);
+            stress_dual_lane(L, e0, r0, j, a, dacol, s0, c0);
+            stress_dual_lane(L, e1, r1, j, yh, dh, sh, chh);
+            stress_dual_lane(L, e1, r1, j, yl, dl, sl, cll);
+            for (int i = 0; i < 6; ++i) tc[i] = scaled_sq(chh[i] - cll[i], c0[i], chh[i], ctl.atol, ctl.rtol);
+            const double pc = group_sum<6>(tc, gmask, gbase);
+            double p = 0.0;
+            for (int i = 0; i < 6; ++i) p += scaled_sq(sh[i] - sl[i], s0[i], sh[i], ctl.atol, ctl.rtol);
+            total = p + pc;
+            count = 42;
+        }
+        double err = sqrt(total / count);
+        if (!(err - err == 0.0) || !ok) err = INFINITY;  // non-finite -> inf (odeint.py:617, 697)
+        const bool accept = err <= 1.0;
+        if (rec_h && j == 0) {  // record_steps (odeint.py:725-727)
+            rec_h[substeps + rejected] = hi;
+            rec_acc[substeps + rejected] = accept ? 1 : 0;
+        }
+        if (accept) {
+            t = clipped ? dt : t + hi;
+            for (int i = 0; i < m; ++i) {
+                a[i] = yh[i];
+                dacol[i] = dh[i];
+            }
+            ++substeps;
+            accepted_any = true;
+        } else {
+            ++rejected;
+        }
+        if constexpr (T::fsal) {  // odeint.py:712-723
+            const int src = accept ? s - 1 : 0;
+            for (int i = 0; i < m; ++i) {
+                g1[i] = G[src][i];
+                gd1[i] = Gd[src][i];
+            }
+            g1_valid = true;
+        }
+        // controller (odeint.py:729-738)
+        double factor = ctl.safety * pow(err, -1.0 / (T::order_low + 1.0));
+        if (err == 0.0) factor = ctl.max_factor;
+        if (factor != factor) factor = ctl.min_factor;
+        factor = fmin(fmax(factor, ctl.min_factor), ctl.max_factor);
+        double hn = hi * factor;
+        if (!accepted_any && !accept) hn = 0.5 * hi;
+        h = hn;
+        const bool done = accept && t >= dt * (1.0 - 1e-12);
+        if (substeps + rejected > ctl.max_substeps) return ST_INTEGRATION;
+        if (done) return 0;
+        if (h < 1e-14 * dt) return ST_INTEGRATION;  // step size underflow
+    }
+}
+#endif  // __CUDACC__
+
 }  // namespace am
