@@ -142,3 +142,44 @@ def test_loading_path_fixtures_are_consistent():
         k = len(g["iterations"])
         np.testing.assert_array_equal(t[1:k + 1], g["time"])
         assert np.array_equal(H.toy_mmc_grid(n).material_ids, g["ids"])
+
+
+def test_python_potentials_match_device_formulas():
+    """The Python potentials (gsm.py:100-256, written over generic scalars
+    like the reference's) are the formulas the device compiles: complex-step
+    derivatives of omega give the oracle's sigma and A = -domega/da, a
+    4th-order difference of psi gives the oracle's f = dpsi/dA."""
+    from oracle import material as OM
+    from paper_2006_04391_b200 import gsm
+
+    rng = np.random.default_rng(3)
+    law = gsm.MichelSuquet()
+    h = 1e-30
+    for _ in range(12):
+        eps = rng.normal(0, 2e-3, 6)
+        a = np.concatenate([rng.normal(0, 5e-4, 6), [abs(rng.normal(0, 1e-3))]])
+        sig, A, f, _, _ = OM.constitutive(OM.ALUMINUM, eps, a)
+        d_eps = [law.omega([complex(x) + (1j * h if i == k else 0) for i, x in enumerate(eps)], list(a)).imag / h
+                 for k in range(6)]
+        d_a = [law.omega(list(eps), [complex(x) + (1j * h if i == k else 0) for i, x in enumerate(a)]).imag / h
+               for k in range(7)]
+        assert np.max(np.abs(np.array(d_eps) - sig)) <= 1e-13 * np.max(np.abs(sig))
+        assert np.max(np.abs(-np.array(d_a) - A)) <= 1e-13 * np.max(np.abs(A))
+        if law.psi(list(A)) <= 0.0:
+            continue  # elastic: f = 0
+        g = []
+        for k in range(7):
+            dk = 1e-4 * max(abs(A[k]), 1e5)
+
+            def ps(t, k=k):
+                x = list(A)
+                x[k] = A[k] + t
+                return law.psi(x)
+
+            g.append((8 * (ps(dk) - ps(-dk)) - (ps(2 * dk) - ps(-2 * dk))) / (12 * dk))
+        assert np.max(np.abs(np.array(g) - f)) <= 1e-7 * np.max(np.abs(f))
+    le = gsm.LinearElastic(300e9, 0.25)
+    eps = rng.normal(0, 1e-3, 6)
+    d = [le.omega([complex(x) + (1j * h if i == k else 0) for i, x in enumerate(eps)], []).imag / h for k in range(6)]
+    assert np.max(np.abs(np.array(d) - le.Ce @ eps)) <= 1e-13 * np.max(np.abs(le.Ce @ eps))
+    assert np.max(np.abs(gsm.DEV6 @ np.arange(6.0) - np.array(gsm.dev_components(list(np.arange(6.0)))))) <= 1e-15
