@@ -363,6 +363,8 @@ def main():
     ap.add_argument("--big-iterations", type=int, default=0,
                     help="config-5 iterations timed on one GPU (0: 300; the full load step on >1 GPU)")
     ap.add_argument("--no-strategies", action="store_true")
+    ap.add_argument("--p2p", action="store_true",
+                    help="at >1 GPU also time config 4 with the fused P2P (CUDA IPC) transposes")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -576,6 +578,11 @@ def main():
             basic[key] = {"error": f"{type(exc).__name__}: {exc}"}
             errors.append(key)
 
+    # a VoxelGrid carries its committed internal state (the reference commits
+    # into grid.state), so every run gets a fresh grid of the same geometry
+    def fresh(g):
+        return H.VoxelGrid(g.material_ids, g.materials)
+
     if args.basic:
         n = args.basic
         grid4 = H.toy_mmc_grid(n)
@@ -583,21 +590,21 @@ def main():
                f"tol 1e-5, {world} GPU(s)")
 
         def c4_step():
-            r = basic_step(grid4, n, dev, dist, comm_of("nccl"))
+            r = basic_step(fresh(grid4), n, dev, dist, comm_of("nccl"))
             r["config"] = {"workload": wl4 + ", load step 1", "parallelism": par("nccl"), "voxels": n**3,
                            "evp_voxels": int(len(grid4.voxel_index[0]))}
-            rw = basic_step(grid4, n, dev, dist, comm_of("nccl"), warm=True)
+            rw = basic_step(fresh(grid4), n, dev, dist, comm_of("nccl"), warm=True)
             r["newton_warm_start"] = {k: rw[k] for k in ("value", "unit", "iterations", "ms_per_iteration",
                                                          "phase_ms_per_iteration")}
             r["newton_warm_start"]["note"] = warm_note
-            if world > 1:
-                rp = basic_step(grid4, n, dev, dist, comm_of("p2p"))
+            if world > 1 and args.p2p:
+                rp = basic_step(fresh(grid4), n, dev, dist, comm_of("p2p"))
                 r["p2p_transport"] = {k: rp[k] for k in ("value", "unit", "iterations", "ms_per_iteration",
                                                          "phase_ms_per_iteration")}
             return r
 
         def c4_path():
-            r = loading_path_run(grid4, dev, dist, comm_of("nccl"))
+            r = loading_path_run(fresh(grid4), dev, dist, comm_of("nccl"))
             r["config"] = {"workload": wl4 + ", all 20 load steps through run_loading_path (reference update per "
                                              "step, tangent sweeps included)", "parallelism": par("nccl")}
             r["note"] = "20-step average: iterations of all steps / wall time of run_loading_path"
@@ -609,10 +616,10 @@ def main():
         grid3 = H.toy_mmc_grid(args.path)
 
         def c3():
-            r = loading_path_run(grid3, dev, dist, comm_of("nccl"))
+            r = loading_path_run(fresh(grid3), dev, dist, comm_of("nccl"))
             r["config"] = {"workload": f"config 3: toy_mmc_grid({args.path}), LoadingPath(steps=20), mixed BC, "
                                        "reference update per step, run_loading_path", "parallelism": par("nccl")}
-            rw = loading_path_run(grid3, dev, dist, comm_of("nccl"), warm=True)
+            rw = loading_path_run(fresh(grid3), dev, dist, comm_of("nccl"), warm=True)
             r["newton_warm_start"] = {k: rw[k] for k in ("value", "unit", "seconds", "iterations_total",
                                                          "sig_xx_final", "C11_final")}
             r["newton_warm_start"]["note"] = warm_note
@@ -625,7 +632,7 @@ def main():
         cap = 5000 if world > 1 else (args.big_iterations or 300)
 
         def c5():
-            r = basic_step(grid5, n, dev, dist, comm_of("nccl"), max_iterations=cap)
+            r = basic_step(fresh(grid5), n, dev, dist, comm_of("nccl"), max_iterations=cap)
             r["config"] = {"workload": f"config 5: toy_mmc_grid({n}, fiber_law=LinearElastic(3000e9, 0.25)) "
                                        f"(~55x contrast), load step 1 of LoadingPath(steps=20), mixed BC, tol 1e-5",
                            "parallelism": par("nccl"), "voxels": n**3}

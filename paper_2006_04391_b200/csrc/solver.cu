@@ -218,83 +218,67 @@ __global__ void k_origin_x(double2* __restrict__ S, double2* __restrict__ ehat, 
     if (threadIdx.x == 0) ehat[c * cs] = make_double2(ebar.v[c] * N, 0.0);
 }
 
-// forward transpose, pack: 2-D spectra P (6, nxl, ny, nzh) -> send blocks
-// [dest j][xl][c][ky - y0_j][kz] (equal ky ranges nyl per slab)
-__global__ void k_pack(const double2* __restrict__ P, double2* __restrict__ send, int nxl, int ny, int nzh, int nyl) {
-    const int64_t total = (int64_t)6 * nxl * ny * nzh;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        // i enumerates the send buffer: ((j * nxl + xl) * 6 + c) * nyl * nzh + kyl * nzh + kz
-        const int kz = (int)(i % nzh);
-        int64_t r = i / nzh;
-        const int kyl = (int)(r % nyl);
-        r /= nyl;
-        const int c = (int)(r % 6);
-        r /= 6;
-        const int xl = (int)(r % nxl);
-        const int j = (int)(r / nxl);
-        const int ky = j * nyl + kyl;
-        send[i] = P[((int64_t)(c * nxl + xl) * ny + ky) * nzh + kz];
-    }
+// Transposes between the x-slab 2-D spectra P (6, nxl, ny, nzh) and the
+// exchange blocks [rank j][xl][c][kyl][kz] (equal ky ranges nyl per slab).
+// For a fixed (j, xl, c) both sides are one contiguous run of nyl * nzh
+// elements, so every kernel is a batch of contiguous copies: block row
+// blockIdx.y = run r = (j * nxl + xl) * 6 + c, threads over the run (no
+// per-element index arithmetic, coalesced 16-byte accesses on both sides).
+__device__ __forceinline__ void run_of(int r, int nxl, int& j, int& xl, int& c) {
+    c = r % 6;
+    xl = (r / 6) % nxl;
+    j = r / (6 * nxl);
 }
 
-// inverse transpose, unpack: receive blocks [src i][xl][c][kyl][kz] -> 2-D
-// spectra P (6, nxl, ny, nzh) with ky = i * nyl + kyl
+// forward transpose, pack: P -> send
+__global__ void k_pack(const double2* __restrict__ P, double2* __restrict__ send, int nxl, int ny, int nzh, int nyl) {
+    int j, xl, c;
+    run_of(blockIdx.y, nxl, j, xl, c);
+    const int64_t len = (int64_t)nyl * nzh;
+    const double2* src = P + ((int64_t)(c * nxl + xl) * ny + (int64_t)j * nyl) * nzh;
+    double2* dst = send + (int64_t)blockIdx.y * len;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+// inverse transpose, unpack: receive blocks [src j][xl][c][kyl][kz] -> P
 __global__ void k_unpack(const double2* __restrict__ recv, double2* __restrict__ P, int nxl, int ny, int nzh, int nyl) {
-    const int64_t total = (int64_t)6 * nxl * ny * nzh;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int kz = (int)(i % nzh);
-        int64_t r = i / nzh;
-        const int kyl = (int)(r % nyl);
-        r /= nyl;
-        const int c = (int)(r % 6);
-        r /= 6;
-        const int xl = (int)(r % nxl);
-        const int src = (int)(r / nxl);
-        const int ky = src * nyl + kyl;
-        P[((int64_t)(c * nxl + xl) * ny + ky) * nzh + kz] = recv[i];
-    }
+    int j, xl, c;
+    run_of(blockIdx.y, nxl, j, xl, c);
+    const int64_t len = (int64_t)nyl * nzh;
+    const double2* src = recv + (int64_t)blockIdx.y * len;
+    double2* dst = P + ((int64_t)(c * nxl + xl) * ny + (int64_t)j * nyl) * nzh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
 }
 
 // Fused transposes over peer memory (NVLink P2P / same-device siblings):
 // the pack kernel stores each destination's block straight into that
-// rank's spectrum buffer (dst[j] + rank * blk ...), so pack and all-to-all
-// are one pass; the inverse reads each source's block straight from that
-// rank's spectrum buffer.  `peer` is a device array of the k ranks' buffers.
+// rank's spectrum buffer (peer[j] + rank * blk + ...), so pack and
+// all-to-all are one pass; the inverse reads each source's block straight
+// from that rank's spectrum buffer.  `peer` is a device array of the k
+// ranks' buffers.
 __global__ void k_pack_peer(const double2* __restrict__ P, double2* const* __restrict__ peer, int rank, int nxl, int ny,
                             int nzh, int nyl) {
-    const int64_t blk = (int64_t)nxl * 6 * nyl * nzh;
-    const int64_t total = (int64_t)6 * nxl * ny * nzh;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int kz = (int)(i % nzh);
-        int64_t r = i / nzh;
-        const int kyl = (int)(r % nyl);
-        r /= nyl;
-        const int c = (int)(r % 6);
-        r /= 6;
-        const int xl = (int)(r % nxl);
-        const int j = (int)(r / nxl);
-        const int ky = j * nyl + kyl;
-        peer[j][rank * blk + (i - j * blk)] = P[((int64_t)(c * nxl + xl) * ny + ky) * nzh + kz];
-    }
+    int j, xl, c;
+    run_of(blockIdx.y, nxl, j, xl, c);
+    const int64_t len = (int64_t)nyl * nzh, blk = (int64_t)nxl * 6 * len;
+    const double2* src = P + ((int64_t)(c * nxl + xl) * ny + (int64_t)j * nyl) * nzh;
+    double2* dst = peer[j] + rank * blk + (int64_t)(xl * 6 + c) * len;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
     __threadfence_system();  // remote stores visible before the barrier that follows
 }
 
 __global__ void k_unpack_peer(double2* const* __restrict__ peer, double2* __restrict__ P, int rank, int nxl, int ny,
                               int nzh, int nyl) {
-    const int64_t blk = (int64_t)nxl * 6 * nyl * nzh;
-    const int64_t total = (int64_t)6 * nxl * ny * nzh;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int kz = (int)(i % nzh);
-        int64_t r = i / nzh;
-        const int kyl = (int)(r % nyl);
-        r /= nyl;
-        const int c = (int)(r % 6);
-        r /= 6;
-        const int xl = (int)(r % nxl);
-        const int src = (int)(r / nxl);
-        const int ky = src * nyl + kyl;
-        P[((int64_t)(c * nxl + xl) * ny + ky) * nzh + kz] = peer[src][rank * blk + (i - src * blk)];
-    }
+    int j, xl, c;
+    run_of(blockIdx.y, nxl, j, xl, c);
+    const int64_t len = (int64_t)nyl * nzh, blk = (int64_t)nxl * 6 * len;
+    const double2* src = peer[j] + rank * blk + (int64_t)(xl * 6 + c) * len;
+    double2* dst = P + ((int64_t)(c * nxl + xl) * ny + (int64_t)j * nyl) * nzh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
 }
 
 // standalone Green application on a single-layout spectrum (GreenOperator.apply):
@@ -639,6 +623,12 @@ static int barrier(am_solver* h) {
     return AM_OK;
 }
 
+// grid of the transpose kernels: one row of blocks per contiguous run
+static dim3 runs_grid(const am_solver* h, const Slab& s) {
+    const int64_t len = (int64_t)s.nyl * h->nzh;
+    return dim3((unsigned)std::min<int64_t>((len + 255) / 256, 64), (unsigned)(h->nslabs * s.nxl * 6));
+}
+
 // ---------------------------------------------------------------- transforms
 // rfft of a real slab field -> spectrum buffer `dst` (S or ehat) of every slab
 static int forward(am_solver* h, double* Slab::*field, double2* Slab::*dst) {
@@ -650,8 +640,8 @@ static int forward(am_solver* h, double* Slab::*field, double2* Slab::*dst) {
     if (h->p2p) {
         for (auto& s : h->slabs) {
             AM_CUFFT(cufftExecD2Z(h->r2, s.*field, s.P));
-            k_pack_peer<<<grid_for((int64_t)6 * s.nxl * h->ny * h->nzh), 256, 0, h->stream>>>(
-                s.P, dst == &Slab::S ? s.peerS : s.peerE, s.rank, s.nxl, h->ny, h->nzh, s.nyl);
+            k_pack_peer<<<runs_grid(h, s), 256, 0, h->stream>>>(s.P, dst == &Slab::S ? s.peerS : s.peerE, s.rank,
+                                                                s.nxl, h->ny, h->nzh, s.nyl);
             AM_CUDA(cudaGetLastError());
         }
         AM_TRY(barrier(h));  // every block has landed
@@ -660,8 +650,7 @@ static int forward(am_solver* h, double* Slab::*field, double2* Slab::*dst) {
     }
     for (auto& s : h->slabs) {
         AM_CUFFT(cufftExecD2Z(h->r2, s.*field, s.P));
-        k_pack<<<grid_for((int64_t)6 * s.nxl * h->ny * h->nzh), 256, 0, h->stream>>>(s.P, s.X, s.nxl, h->ny, h->nzh,
-                                                                                      s.nyl);
+        k_pack<<<runs_grid(h, s), 256, 0, h->stream>>>(s.P, s.X, s.nxl, h->ny, h->nzh, s.nyl);
         AM_CUDA(cudaGetLastError());
     }
     AM_TRY(alltoall(h, &Slab::X, dst, (size_t)6 * h->slabs[0].nxl * h->slabs[0].nyl * h->nzh));
@@ -680,8 +669,8 @@ static int inverse(am_solver* h, double2* Slab::*src, double* Slab::*field) {
     if (h->p2p) {
         AM_TRY(barrier(h));  // every rank's x-transform is done before it is read
         for (auto& s : h->slabs) {
-            k_unpack_peer<<<grid_for((int64_t)6 * s.nxl * h->ny * h->nzh), 256, 0, h->stream>>>(
-                src == &Slab::S ? s.peerS : s.peerE, s.P, s.rank, s.nxl, h->ny, h->nzh, s.nyl);
+            k_unpack_peer<<<runs_grid(h, s), 256, 0, h->stream>>>(src == &Slab::S ? s.peerS : s.peerE, s.P, s.rank,
+                                                                  s.nxl, h->ny, h->nzh, s.nyl);
             AM_CUDA(cudaGetLastError());
         }
         AM_TRY(barrier(h));  // nobody overwrites a spectrum a peer is still reading
@@ -690,8 +679,7 @@ static int inverse(am_solver* h, double2* Slab::*src, double* Slab::*field) {
     }
     AM_TRY(alltoall(h, src, &Slab::X, (size_t)6 * h->slabs[0].nxl * h->slabs[0].nyl * h->nzh));
     for (auto& s : h->slabs) {
-        k_unpack<<<grid_for((int64_t)6 * s.nxl * h->ny * h->nzh), 256, 0, h->stream>>>(s.X, s.P, s.nxl, h->ny,
-                                                                                        h->nzh, s.nyl);
+        k_unpack<<<runs_grid(h, s), 256, 0, h->stream>>>(s.X, s.P, s.nxl, h->ny, h->nzh, s.nyl);
         AM_CUDA(cudaGetLastError());
         AM_CUFFT(cufftExecZ2D(h->c2, s.P, s.*field));
     }

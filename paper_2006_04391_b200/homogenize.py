@@ -23,6 +23,7 @@ handling, as in the reference.
 
 import ctypes
 import json
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -86,7 +87,11 @@ class VoxelGrid:
     """Periodic voxel grid with per-voxel material ids and internal state (homogenize.py:85-107).
 
     While a ``Homogenizer`` is bound to the grid the authoritative internal
-    state lives on the device; ``state`` is fetched from there on access.
+    state lives on the device; ``state`` is fetched from there on access
+    (and copied back when the solver is released), so the grid carries the
+    committed state like the reference's in-place commits (homogenize.py:474-480).
+    The grid references its solver weakly: releasing the Homogenizer frees
+    its device memory.
     """
 
     def __init__(self, material_ids, materials):
@@ -101,12 +106,13 @@ class VoxelGrid:
             raise ValueError("material id exceeds material table")
         self.voxel_index = [np.flatnonzero(ids_flat == mid) for mid in range(len(self.materials))]
         self._state = [np.zeros((len(idx), law.m)) for idx, law in zip(self.voxel_index, self.materials)]
-        self._solver = None  # Homogenizer whose device state is authoritative
+        self._solver = None  # weakref to the Homogenizer whose device state is authoritative
 
     @property
     def state(self):
-        if self._solver is not None:
-            self._solver._pull_state(self._state)
+        solver = self._solver() if self._solver is not None else None
+        if solver is not None:
+            solver._pull_state(self._state)
         return self._state
 
     @property
@@ -116,8 +122,9 @@ class VoxelGrid:
     def reset_state(self):
         for arr in self._state:
             arr[:] = 0.0
-        if self._solver is not None:
-            self._solver._push_state(self._state)
+        solver = self._solver() if self._solver is not None else None
+        if solver is not None:
+            solver._push_state(self._state)
 
 
 def toy_mmc_grid(n=16, matrix_law=None, fiber_law=None, volume_fraction=0.10, seed=2024):
@@ -312,7 +319,7 @@ class Homogenizer:
         self._last = None  # (eps, ebar) host arrays of the last converged step
         if comm is None:
             self._push_state(grid._state)
-            grid._solver = self
+            grid._solver = weakref.ref(self)
         else:
             self._push_state(self._local_states(grid._state))
         self.reference = None
@@ -321,6 +328,13 @@ class Homogenizer:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _lib._LIB is not None:
+            grid = getattr(self, "grid", None)
+            ref = grid._solver if grid is not None else None
+            if ref is not None and self.comm is None and ref() in (None, self):
+                try:  # the grid keeps the committed state (the solver is going away)
+                    self._pull_state(grid._state)
+                except Exception:  # noqa: BLE001 - best effort during teardown
+                    pass
             _lib._LIB.am_solver_destroy(h)
             self._h = None
 
