@@ -18,17 +18,18 @@ from . import _lib
 class Comm:
     """Rank, world size and the NCCL unique id of a communicator to create.
 
-    ``allgather`` (bytes -> list of every rank's bytes) lets the solver swap
-    CUDA IPC handles so the transposes run as fused pack / unpack kernels
-    over NVLink peer memory; ``transport`` = "p2p" (default when
-    ``allgather`` is given) or "nccl" (ncclAlltoAll).
+    ``transport`` = "nccl" (default: ncclAlltoAll transposes, the north
+    star's path) or "p2p" (opt-in: fused pack / unpack kernels over NVLink
+    peer memory through CUDA IPC handles swapped with ``allgather``, bytes
+    -> list of every rank's bytes; tested on sibling slabs of one GPU and at
+    world size 1 -- a multi-process run needs a multi-GPU box).
     """
 
     rank: int
     world: int
     uid: bytes
     allgather: Optional[Callable[[bytes], list]] = None
-    transport: str = "p2p"
+    transport: str = "nccl"
 
 
 def nccl_unique_id():
@@ -39,7 +40,7 @@ def nccl_unique_id():
     return buf.raw
 
 
-def comm_from_torch(group=None, transport="p2p"):
+def comm_from_torch(group=None, transport="nccl"):
     """Build a Comm over an initialised torch.distributed process group:
     rank 0 creates the NCCL id, the group broadcasts it (and later the IPC
     handles of the P2P transport)."""

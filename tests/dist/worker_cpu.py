@@ -40,6 +40,15 @@ def main():
         dist.all_reduce(t)
         whole = M.plane_partials(ref.transpose(1, 0, 2, 3), 0, ny, nz // 2 + 1)
         assert np.array_equal(t.numpy(), whole), "reduction slots depend on the slab count"
+        # 4. plane-ordered field means (eps.mean(), sigma_bar) and C_bar records
+        # (solver.cu field_means / k_refstats_planes): each rank fills the
+        # records of its own x planes, zeros elsewhere; the all-reduce is
+        # exact and the plane-ordered sum equals the one-rank result bitwise
+        pl = np.zeros((nx, 6))
+        pl[x0:x1] = g[:, x0:x1].sum(axis=(2, 3)).T
+        t = torch.from_numpy(pl)
+        dist.all_reduce(t)
+        assert np.array_equal(t.numpy(), g.sum(axis=(2, 3)).T), "plane records depend on the slab count"
     dist.barrier()
     if r == 0:
         print("WORKER-OK", flush=True)
