@@ -207,14 +207,17 @@ __global__ void __launch_bounds__(128, AM_LANES_MINB) k_adaptive_lanes(Law L, KA
         int sub = 1, rej = 0, st = 0;
         if (dt == 0.0) {  // frozen (evaluator.py:142-150): a_n, elastic tangent, no clamp
             for (int i = 0; i < m; ++i) ac[i] = an[i];
-            stress_dual_lane(L, ep, 1.0, j, an, nullptr, sig, ccol);
+            if constexpr (is_semi_v<Law>) semi_stress_tangent_cols(L, ep, an, nullptr, 1, j, sig, ccol);
+            else stress_dual_lane(L, ep, 1.0, j, an, nullptr, sig, ccol);
         } else {
             double* rh = k.rec_h ? k.rec_h + k.rec_off[b] : nullptr;
             uint8_t* ra = k.rec_h ? k.rec_acc + k.rec_off[b] : nullptr;
             st = adaptive_point_lanes<Law, Scheme>(L, k.sctl, en, an, ep, dt, a, dacol, sub, rej, j, gmask, gbase, rh,
                                                    ra);
-            clamp_state<Law>(a, ac);                              // evaluator.py:198
-            stress_dual_lane(L, ep, 1.0, j, ac, dacol, sig, ccol);  // evaluator.py:200
+            clamp_state<Law>(a, ac);  // evaluator.py:198
+            // evaluator.py:200 (semi-automatic: the hand-coded tangent, gsm.py:553-560)
+            if constexpr (is_semi_v<Law>) semi_stress_tangent_cols(L, ep, ac, dacol, 1, j, sig, ccol);
+            else stress_dual_lane(L, ep, 1.0, j, ac, dacol, sig, ccol);
         }
         bool fin = true;
 #pragma unroll
@@ -278,7 +281,7 @@ int launch_adaptive(const Law& L, const KArgs& k, unsigned g, cudaStream_t s) {
     // lane groups for ode23 (automatic): 26.3 vs 21.0 M evals/s (internal
     // measure), 12.9 vs 8.6 (stress); ode12's unrolled one-thread kernel
     // stays faster (12.3 vs 7.1) -- k1_variants.log, round 2
-    if (k.C && AM_ADAPT_LANES && !is_semi_v<Law> && Scheme == 23) {
+    if (k.C && AM_ADAPT_LANES && Scheme == 23) {
         int64_t blocks = (k.B + 19) / 20;  // 4 warps x 5 points
         if (blocks > (int64_t)kSMs * 512) blocks = (int64_t)kSMs * 512;
         k_adaptive_lanes<Law, Scheme><<<(unsigned)blocks, 128, 0, s>>>(L, k);
