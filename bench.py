@@ -453,14 +453,29 @@ def main():
     iters = d_it.cpu().numpy()
     fl = float(np.sum(flops_per_eval(iters.astype(np.float64))))
     achieved = fl / (ms * 1e-3) / 1e12
-    traffic = None
+    traffic = traffic_newton = traffic_tangent = None
     try:  # DRAM bytes per point of the two K1 kernels from the committed ncu capture
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic.json")))
-        traffic = B * (tj["k_material_newton_raw_bytes_per_point"] + tj["k_tangent_bytes_per_point"])
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r02", "traffic.json")))
+        traffic_newton = B * tj["k_material_newton_raw_bytes_per_point"]
+        traffic_tangent = B * tj["k_tangent_bytes_per_point"]
+        traffic = traffic_newton + traffic_tangent
     except (OSError, KeyError, ValueError):
         pass
     peak = ctypes.c_double(0.0)
     _lib.check(lib.am_probe_fp64_tflops(5, ctypes.byref(peak)))
+    # per-kernel device times of the same launches (CUDA events around the
+    # Newton and the tangent kernel on this stream; a separate pass, since
+    # the events synchronise after every launch)
+    kt = np.zeros(3)
+    _lib.check(lib.am_k1_timing(1, None))
+    for _ in range(max(3, args.steps)):
+        step()
+    torch.cuda.synchronize()
+    _lib.check(lib.am_k1_timing(-1, _lib.ptr(kt)))
+    _lib.check(lib.am_k1_timing(0, None))
+    t_newton, t_tangent = kt[0] / kt[2], kt[1] / kt[2]
+    fl_newton = float(np.sum(1072.0 * iters.astype(np.float64) + 18.0))  # raw Newton: + delta eps, eps(t1)
+    fl_tangent = 2255.0 * B  # tangent post-process 1695 + stress 20 + C 540
 
     # ---- the paper's strategy comparison on the same batch (stress + tangent,
     # device-resident): every strategy x integrator route the reference offers
@@ -658,13 +673,28 @@ def main():
                    "batch_per_gpu": B, "parallelism": f"dp{world} (independent points, no collective)",
                    "l2": "inputs+outputs 552 MiB per step > 126 MB L2 (no flush needed)",
                    "mean_newton_iters": float(iters.mean())},
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                     "frac": achieved / peak.value if peak.value else None, "traffic": traffic,
-                     "traffic_source": "ncu dram bytes per point (profiles/r01/traffic.json) x points per step",
+        "roofline": {"bound": "fp64", "kernel": "k_material<MichelSuquetLaw> (Newton, the dominant kernel)",
+                     "achieved": fl_newton / (t_newton * 1e-3) / 1e12, "peak": peak.value, "unit": "TFLOP/s",
+                     "frac": fl_newton / (t_newton * 1e-3) / 1e12 / peak.value if peak.value else None,
+                     "traffic": traffic_newton,
+                     "traffic_source": "ncu dram__bytes_read + dram__bytes_write of this kernel per point "
+                                       "(profiles/r02/traffic.json) x points per launch",
                      "peak_source": "measured: am_probe_fp64_tflops DFMA microbenchmark on this GPU "
                                     "(MEASURED_PEAKS.json has no fp64 entry)",
-                     "work_per_launch": f"{fl:.4g} algorithmic fp64 flops per step (SURVEY §8d: 1072*N_it + 2273 per eval); "
-                                        "one step = the Newton kernel + the tangent kernel"},
+                     "work_per_launch": f"{fl_newton:.4g} algorithmic fp64 flops per launch (1072 per Newton "
+                                        "iteration of each point + 18, SURVEY §8d)",
+                     "launch_ms": t_newton, "share_of_step": t_newton / (t_newton + t_tangent),
+                     "timing": "CUDA events around each kernel on the launching stream (am_k1_timing), "
+                               f"{int(kt[2])} launches",
+                     "tangent_kernel": {"kernel": "k_tangent<MichelSuquetLaw>", "launch_ms": t_tangent,
+                                        "achieved": fl_tangent / (t_tangent * 1e-3) / 1e12,
+                                        "frac": fl_tangent / (t_tangent * 1e-3) / 1e12 / peak.value,
+                                        "work_per_launch": f"{fl_tangent:.4g} flops (2255 per point)",
+                                        "traffic": traffic_tangent},
+                     "step": {"achieved": achieved, "frac": achieved / peak.value if peak.value else None,
+                              "traffic": traffic,
+                              "work_per_step": f"{fl:.4g} flops (1072*N_it + 2273 per eval); one step = the "
+                                               "Newton kernel + the tangent kernel"}},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "evaluator.evaluate_arrays (the reference's drop-in call) with the caller's pageable numpy "
                         "arrays -> am_eval_batch_host: pinned staging of the inputs by a host copy pool, results "

@@ -122,6 +122,13 @@ int am_eval_batch(const am_law *law, const am_cfg *cfg, int64_t B,
                   double *sigma, double *a_out, double *C,
                   int32_t *newton_iters, int32_t *rejected, uint8_t *status, uint32_t *flags, void *stream);
 
+/* Per-kernel device time of the stress + tangent route (Newton kernel,
+ * tangent kernel), from CUDA events on the launching stream around each
+ * kernel (synchronises after every launch while on: a measurement mode).
+ * enable 1 = on (reset), 0 = off, -1 = query; out (3, optional) = Newton
+ * ms, tangent ms, launches.  No reference counterpart (roofline evidence). */
+int am_k1_timing(int enable, double *out);
+
 /*
  * am_eval_batch_host -- same as evaluate_arrays with the reference's host
  * AoS arrays: eps_n/eps_np1 (B,6), a_n/a_out (B,m), dt (B), sigma (B,6),

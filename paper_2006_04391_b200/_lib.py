@@ -96,6 +96,7 @@ SIGNATURES = {
     ]),
     "am_probe_fp64_tflops": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "am_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "am_k1_timing": (ctypes.c_int, [ctypes.c_int, _dp]),
     "am_host_free": (ctypes.c_int, [_vp]),
     "am_lawops_host": (ctypes.c_int, [
         ctypes.POINTER(am_law), ctypes.c_int, ctypes.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,

@@ -15,6 +15,7 @@ namespace am {
 
 // default-pool release threshold (material.cu)
 void keep_pool_memory();
+void k1_mark(int i, cudaStream_t s);  // am_k1_timing events (material.cu)
 
 // writes C[i][j] of item `off` to C[(i * 6 + j) * cs + off]
 struct GlobalSink {
@@ -322,6 +323,7 @@ int launch_law(const Law& L, KArgs k, cudaStream_t s) {
         AM_CUDA(cudaMallocAsync((void**)&scratch, (size_t)k.B, s));
         k.status = scratch;
     }
+    k1_mark(0, s);
     if (Law::m > 0) {
         KArgs kn = k;
         kn.flags = nullptr;  // the tangent kernel reports the combined status
@@ -329,8 +331,10 @@ int launch_law(const Law& L, KArgs k, cudaStream_t s) {
         else k_material<Law, 0, true><<<g, threads, 0, s>>>(L, kn);
         AM_CUDA(cudaGetLastError());
     }
+    k1_mark(1, s);
     k_tangent<Law><<<g, threads, 0, s>>>(L, k);
     AM_CUDA(cudaGetLastError());
+    k1_mark(2, s);
     if (scratch) AM_CUDA(cudaFreeAsync(scratch, s));
     return AM_OK;
 }

@@ -178,6 +178,38 @@ void keep_pool_memory() {
     done.push_back(dev);
 }
 
+// Per-kernel device time of the two-kernel tangent route (am_k1_timing):
+// events before the Newton kernel, between the kernels and after the
+// tangent kernel, on the launching stream.
+namespace {
+struct K1Timing {
+    bool on = false;
+    cudaEvent_t e[3] = {};
+    double ms[2] = {0.0, 0.0};
+    int64_t launches = 0;
+    std::mutex mu;
+};
+K1Timing& k1_timing() {
+    static K1Timing t;
+    return t;
+}
+}  // namespace
+
+void k1_mark(int i, cudaStream_t s) {
+    K1Timing& t = k1_timing();
+    if (!t.on) return;
+    cudaEventRecord(t.e[i], s);
+    if (i == 2) {
+        float a = 0.f, b = 0.f;
+        cudaEventSynchronize(t.e[2]);
+        cudaEventElapsedTime(&a, t.e[0], t.e[1]);
+        cudaEventElapsedTime(&b, t.e[1], t.e[2]);
+        t.ms[0] += a;
+        t.ms[1] += b;
+        ++t.launches;
+    }
+}
+
 int launch_material(const am_law* law, const KArgs& k, cudaStream_t s) {
     if (k.B == 0) return AM_OK;
     const bool semi = k.strategy == AM_STRATEGY_SEMI_AUTOMATIC || k.strategy == AM_STRATEGY_CONVENTIONAL;
@@ -203,6 +235,24 @@ int law_m(const am_law* law) { return law->kind == AM_LAW_MICHEL_SUQUET ? 7 : 0;
 }  // namespace am
 
 using namespace am;
+
+extern "C" int am_k1_timing(int enable, double* out) {
+    K1Timing& t = k1_timing();
+    std::lock_guard<std::mutex> lk(t.mu);
+    if (enable >= 0) {
+        if (enable && !t.e[0])
+            for (auto& e : t.e) AM_CUDA(cudaEventCreate(&e));
+        t.on = enable != 0;
+        t.ms[0] = t.ms[1] = 0.0;
+        t.launches = 0;
+    }
+    if (out) {
+        out[0] = t.ms[0];
+        out[1] = t.ms[1];
+        out[2] = (double)t.launches;
+    }
+    return AM_OK;
+}
 
 extern "C" int am_eval_batch(const am_law* law, const am_cfg* cfg, int64_t B, const double* eps_n,
                              const double* a_n, const double* eps_np1, const double* dt, double dt_scalar,
