@@ -126,6 +126,40 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def gsmkit_rates():
+    """The reference package itself (gsmkit, installed unmodified in
+    baseline/_ref by __graft_entry__.build()) on small config-2 samples:
+    evaluate_arrays on the automatic route (threads = 1 and all host
+    threads; GIL-bound) and the conventional radial return, the reference's
+    fastest CPU route.  Informational keys of the
+    reference line; None when baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(ref, "gsmkit", "evaluator.py")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        from gsmkit import gsm as rg
+        from gsmkit.evaluator import StrategyConfig as RSC, evaluate_arrays as rev
+    finally:
+        sys.path.remove(ref)
+    from paper_2006_04391_b200.workloads import config2_batch
+
+    out = {}
+    threads = os.cpu_count() or 1
+    for key, strat, n, thr in (("automatic_1_thread", "automatic", 1 << 12, 1),
+                               (f"automatic_{threads}_threads", "automatic", 1 << 13, threads),
+                               ("conventional_1_thread", "conventional", 1 << 16, 1)):
+        en, an, ep, dt = config2_batch(n, seed=0)
+        cfg = RSC(strategy=strat, integrator="implicit-euler")
+        t0 = time.perf_counter()
+        rev(rg.MichelSuquet(), cfg, en, an, ep, dt, want_tangent=True, threads=thr)
+        out[key] = {"evals_per_s": n / (time.perf_counter() - t0), "points": n}
+    out["note"] = ("gsmkit (the unmodified reference, Python + numpy) from baseline/_ref, stress + tangent, "
+                   "config-2 sample; the reference arm's value is the C restatement of the automatic route "
+                   "(kind: port, all host threads), the faster of the two implementations of this path")
+    return out
+
+
 def run_reference(args, rank):
     """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
     if rank != 0:
@@ -153,6 +187,10 @@ def run_reference(args, rank):
                                    f"{threads} threads, {cpu_model()}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        line["gsmkit"] = gsmkit_rates()
+    except Exception as exc:  # noqa: BLE001 - informational only
+        line["gsmkit"] = {"error": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line), flush=True)
 
 
