@@ -40,7 +40,10 @@
 namespace am {
 
 constexpr int kXN = 256;                 // supported nx
-constexpr int kXJ = 2;                   // (ky, kz) columns per tile
+#ifndef AM_XF_J
+#define AM_XF_J 2
+#endif
+constexpr int kXJ = AM_XF_J;             // (ky, kz) columns per tile
 constexpr int kXLines = 6 * kXJ;         // lines per tile
 constexpr int kXThreads = kXLines * 16;  // 16 threads per line: 192
 #ifndef AM_XF_CTAS
