@@ -145,6 +145,34 @@ __device__ __forceinline__ void line_fft256(double2* line, const double2* tw, in
     __syncwarp();
 }
 
+// 16-byte asynchronous global -> shared copy; zero fill when !valid
+__device__ __forceinline__ void cp_async16(double2* dst, const double2* src, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+#ifndef AM_XF_PREFETCH
+#define AM_XF_PREFETCH 0
+#endif
+constexpr int kXNB = AM_XF_PREFETCH ? 2 : 1;  // tile buffers (2: the next tile prefetched with cp.async)
+
+// stage tile `tile` of the 2-D spectra into buf (asynchronous)
+__device__ __forceinline__ void xtile_prefetch(double2* buf, const double2* __restrict__ S, int64_t cs, int64_t ncol,
+                                               int64_t tile) {
+    const int64_t j0 = tile * kXJ;
+#pragma unroll
+    for (int r = 0; r < kXLines * kXN / kXThreads; ++r) {
+        const int e = threadIdx.x + r * kXThreads;
+        const int jj = e & (kXJ - 1), x = (e / kXJ) & (kXN - 1), c = e / (kXJ * kXN);
+        const int64_t j = j0 + jj;
+        cp_async16(buf + (c * kXJ + jj) * kXRow + xpos(x), S + (j < ncol ? c * cs + x * ncol + j : 0), j < ncol);
+    }
+}
+
 // Persistent: CTA b handles tiles b, b + grid, ...  red[tile] = the tile's
 // residual partial; red[P + c] = Re sigma_hat(origin) (the caller zeroes the
 // slots).  S: 2-D spectra (c, x, j) in, 2-D spectra of the next eps (without
@@ -153,7 +181,7 @@ __global__ void __launch_bounds__(kXThreads, kXCtas) k_xfourier(int nx, int ny, 
                                                                 double2* __restrict__ S, double2* __restrict__ ehat,
                                                                 double* __restrict__ red, int64_t P) {
     extern __shared__ double2 xsm[];
-    double2* tw = xsm + kXLines * kXRow;  // [256]
+    double2* tw = xsm + kXNB * kXLines * kXRow;  // [256]
     __shared__ double rsh[kXThreads / 32];
     const int nzh = nz / 2 + 1;
     const int64_t ncol = (int64_t)ny * nzh;  // = x stride of the 2-D spectra
@@ -165,19 +193,33 @@ __global__ void __launch_bounds__(kXThreads, kXCtas) k_xfourier(int nx, int ny, 
         tw[m] = make_double2(c, s);
     }
     const int L = t >> 4, i = t & 15;  // line L = c * kXJ + jj
-    double2* line = xsm + L * kXRow;
     const double invN = 1.0 / ((double)nx * ny * nz);
     constexpr int kE = kXLines * kXN / kXThreads;  // tile elements per thread: 16
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (kXNB == 2) {
+        if (blockIdx.x < ntiles) xtile_prefetch(xsm, S, cs, ncol, blockIdx.x);
+        cp_async_commit();
+    }
+    int cur = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, cur ^= (kXNB - 1)) {
         const int64_t j0 = tile * kXJ;
-        // load: element e -> (c, x, jj), consecutive threads take the two
-        // columns of one (c, x) row (a 32-byte sector)
+        double2* xs = xsm + cur * kXLines * kXRow;  // this tile's lines
+        double2* line = xs + L * kXRow;
+        if constexpr (kXNB == 2) {
+            // the next tile streams in while this one is transformed
+            if (tile + gridDim.x < ntiles) xtile_prefetch(xsm + (cur ^ 1) * kXLines * kXRow, S, cs, ncol, tile + gridDim.x);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            // load: element e -> (c, x, jj), consecutive threads take the
+            // columns of one (c, x) row
 #pragma unroll
-        for (int r = 0; r < kE; ++r) {
-            const int e = t + r * kXThreads;
-            const int jj = e & (kXJ - 1), x = (e / kXJ) & (kXN - 1), c = e / (kXJ * kXN);
-            const int64_t j = j0 + jj;
-            xsm[(c * kXJ + jj) * kXRow + xpos(x)] = j < ncol ? __ldg(S + c * cs + x * ncol + j) : make_double2(0.0, 0.0);
+            for (int r = 0; r < kE; ++r) {
+                const int e = t + r * kXThreads;
+                const int jj = e & (kXJ - 1), x = (e / kXJ) & (kXN - 1), c = e / (kXJ * kXN);
+                const int64_t j = j0 + jj;
+                xs[(c * kXJ + jj) * kXRow + xpos(x)] =
+                    j < ncol ? __ldg(S + c * cs + x * ncol + j) : make_double2(0.0, 0.0);
+            }
         }
         __syncthreads();
         line_fft256<-1>(line, tw, i);
@@ -190,7 +232,7 @@ __global__ void __launch_bounds__(kXThreads, kXCtas) k_xfourier(int nx, int ny, 
             if (j >= ncol) continue;
             const int ky = (int)(j / nzh), kz = (int)(j - (int64_t)ky * nzh);
             const Bin bn = make_bin(kx, ky, kz, nx, ny, nz);
-            double2* cell = xsm + jj * kXRow + xpos(kx);  // component c at cell[c * kXJ * kXRow]
+            double2* cell = xs + jj * kXRow + xpos(kx);  // component c at cell[c * kXJ * kXRow]
             cplx s[6];
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
@@ -246,12 +288,13 @@ __global__ void __launch_bounds__(kXThreads, kXCtas) k_xfourier(int nx, int ny, 
             const int e = t + r * kXThreads;
             const int jj = e & (kXJ - 1), x = (e / kXJ) & (kXN - 1), c = e / (kXJ * kXN);
             const int64_t j = j0 + jj;
-            if (j < ncol) S[c * cs + x * ncol + j] = xsm[(c * kXJ + jj) * kXRow + xpos(x)];
+            if (j < ncol) S[c * cs + x * ncol + j] = xs[(c * kXJ + jj) * kXRow + xpos(x)];
         }
         __syncthreads();  // the lines are read before the next tile overwrites them
     }
+    if constexpr (kXNB == 2) cp_async_wait<0>();
 }
 
-constexpr size_t kXSmem = sizeof(double2) * (kXLines * kXRow + kXN);
+constexpr size_t kXSmem = sizeof(double2) * (kXNB * kXLines * kXRow + kXN);
 
 }  // namespace am
