@@ -695,6 +695,37 @@ def main():
     if world == 1 and args.basic:
         guarded("config1", lambda: config1_run(dev))
 
+        def slab_alg():
+            # the multi-GPU algorithm (2-D FFTs, 8 x-slab transposes as device
+            # copies, 1-D FFTs over x) on this one GPU: same iterations, and the
+            # per-iteration cost of the decomposition itself
+            hom = H.Homogenizer(fresh(grid4), cfg, slabs=8)
+            stream = _solver_stream(hom, dev)
+            path = H.LoadingPath(steps=20)
+            t = path.times()
+            target = np.zeros(6)
+            target[0] = path.eps_xx(t)[1]
+            _lib.check(hom._lib.am_solver_timing(hom._h, 1, None))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            info, _ = hom._solve(target, t[1] - t[0], FREE)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            ph = np.zeros(5)
+            _lib.check(hom._lib.am_solver_timing(hom._h, -1, _lib.ptr(ph)))
+            k = ph[4] or 1.0
+            return {"value": info.iterations / (ms * 1e-3), "unit": "it/s", "iterations": info.iterations,
+                    "ms_per_iteration": ms / info.iterations,
+                    "phase_ms_per_iteration": {"material": ph[0] / k, "forward_fft+transpose": ph[1] / k,
+                                               "fourier+reduce": ph[2] / k,
+                                               "origin+inverse_fft+transpose": ph[3] / max(k - 1, 1)},
+                    "config": {"workload": f"config 4 grid, load step 1, 8 x-slabs of one GPU (am_solver_create_slabs: "
+                                           "the multi-GPU algorithm with device-copy transposes)"}}
+
+        guarded("config4_step1_slab_algorithm", slab_alg)
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
