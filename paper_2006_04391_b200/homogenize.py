@@ -111,8 +111,9 @@ class VoxelGrid:
     @property
     def state(self):
         solver = self._solver() if self._solver is not None else None
-        if solver is not None:
+        if solver is not None and solver._state_dirty:
             solver._pull_state(self._state)
+            solver._state_dirty = False
         return self._state
 
     @property
@@ -317,6 +318,7 @@ class Homogenizer:
             _lib.check(self._lib.am_solver_ipc_import(h, b"".join(every), comm.world), "ipc import")
         self._ebar_n = np.zeros(6)
         self._last = None  # (eps, ebar) host arrays of the last converged step
+        self._state_dirty = False  # committed device state newer than grid._state
         if comm is None:
             self._push_state(grid._state)
             grid._solver = weakref.ref(self)
@@ -330,7 +332,7 @@ class Homogenizer:
         if h is not None and h.value and _lib._LIB is not None:
             grid = getattr(self, "grid", None)
             ref = grid._solver if grid is not None else None
-            if ref is not None and self.comm is None and ref() in (None, self):
+            if ref is not None and self.comm is None and ref() in (None, self) and getattr(self, "_state_dirty", False):
                 try:  # the grid keeps the committed state (the solver is going away)
                     self._pull_state(grid._state)
                 except Exception:  # noqa: BLE001 - best effort during teardown
@@ -473,6 +475,7 @@ class Homogenizer:
             self._set(0, eps)
         self._ebar_n = np.array(ebar, dtype=float)
         _lib.check(self._lib.am_solver_commit(self._h, _lib.ptr(self._ebar_n)))
+        self._state_dirty = True
         self._last = None
 
 
@@ -512,6 +515,7 @@ def run_loading_path(grid, path, cfg, update_reference=True, threads=1, tol=1e-5
         else:
             hom._ebar_n = ebar
             _lib.check(lib.am_solver_commit(hom._h, _lib.ptr(ebar)))
+        hom._state_dirty = True
         if k == len(times) - 1 and comm is None:
             hom.grid.state  # noqa: B018  (refresh the host copy of the final state)
         records.append({

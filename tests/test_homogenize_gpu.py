@@ -371,3 +371,22 @@ def test_slab_count_must_divide(H, AUTO):
     grid = H.VoxelGrid(np.zeros((6, 6, 4), dtype=np.uint8), [gsm.LinearElastic(1e9, 0.3)])
     with pytest.raises(ValueError):
         H.Homogenizer(grid, AUTO, slabs=4)
+
+
+def test_grid_keeps_committed_state(H, AUTO):
+    """The grid carries the committed state like the reference's in-place
+    commits: after run_loading_path (whose solver is released) grid.state is
+    the final state, and a new Homogenizer on the grid starts from it."""
+    g8 = H.toy_mmc_grid(8)
+    recs = H.run_loading_path(g8, H.LoadingPath(steps=20), AUTO)
+    final = [a.copy() for a in g8.state]
+    assert np.max(np.abs(final[0])) > 0.0
+    hom = H.Homogenizer(g8, AUTO)
+    assert rel(g8.state[0], final[0]) == 0.0
+    eb = np.zeros(6)
+    eb[0] = recs[-1]["eps_xx"]
+    eps, sig, info = hom.solve_step(eb, 0.1, free_mask=np.array([False] + [True] * 5))
+    hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+    committed = [a.copy() for a in g8.state]
+    del hom  # released: the grid keeps what was committed
+    assert rel(g8.state[0], committed[0]) == 0.0
