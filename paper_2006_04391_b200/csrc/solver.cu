@@ -539,7 +539,8 @@ struct am_solver {
     double* dsmall = nullptr;     // nccl reductions of the tangent statistics
     double* pl = nullptr;         // per-plane sums of eps and sigma (2 x nx x 6), field_means
     double* hpl = nullptr;        // pinned host copy
-    int64_t nstat = 0;            // tangent statistics records: nmat x nx x kSParts
+    int64_t nstat = 0;            // tangent statistics records: present phases x nx x kSParts
+    std::vector<int> phase_rec;   // record block of each phase (phases without voxels: -1)
     double* ps = nullptr;         // per-(phase, x plane, part) records of k_refstats_planes
     double* hps = nullptr;        // pinned host copy
     bool p2p = false;             // fused pack / unpack over peer memory instead of the all-to-all
@@ -886,7 +887,15 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
     AMC(cudaMalloc(&h->dsmall, sizeof(double) * 64));
     AMC(cudaMalloc(&h->pl, sizeof(double) * 12 * nx));
     AMC(cudaMallocHost(&h->hpl, sizeof(double) * 12 * nx));
-    h->nstat = (int64_t)nmat * nx * kSParts;
+    {  // records only for phases that have voxels somewhere in the grid
+        std::vector<int64_t> cnt(nmat, 0);
+        for (int64_t i = 0; i < N; ++i) ++cnt[ids[i]];
+        int np = 0;
+        h->phase_rec.assign(nmat, -1);
+        for (int k = 0; k < nmat; ++k)
+            if (cnt[k]) h->phase_rec[k] = np++;
+        h->nstat = (int64_t)std::max(np, 1) * nx * kSParts;
+    }
     AMC(cudaMalloc(&h->ps, sizeof(double) * kStat * h->nstat));
     AMC(cudaMallocHost(&h->hps, sizeof(double) * kStat * h->nstat));
 #undef AMC
@@ -1303,7 +1312,7 @@ extern "C" int am_solver_tangent_sweep(am_solver* h, double dt, double* Cbar, do
                     k.iters = nullptr; k.status = h->status; k.flags = s.flags;
                     set_controls(k, &h->cfg);
                     AM_TRY(launch_material(&p.law, k, h->stream));
-                    const int64_t rec = ((int64_t)ip * h->nx + s.x0 + xa) * kSParts;
+                    const int64_t rec = ((int64_t)h->phase_rec[ip] * h->nx + s.x0 + xa) * kSParts;
                     k_refstats_planes<<<(unsigned)((xb - xa) * kSParts), kRedThreads, 0, h->stream>>>(
                         h->Cbuf, n, p.dpoff, xa, lo, h->db, dsum + rec * kSum, dmin + rec * 4);
                     AM_CUDA(cudaGetLastError());
