@@ -553,6 +553,47 @@ def make_path8_ode23_fail():
     save("path8_ode23_fail.npz", **out)
 
 
+def make_radial_stall():
+    """A Michel-Suquet parameter set (n = 10, small sigma_d) whose radial
+    return stalls (gsm.py:377-378 NewtonError) at eps_n = 0, a_n = 0: the
+    reference raises from conventional_evaluate, from evaluate_arrays with
+    strategy="conventional" and from Homogenizer.solve_step on a homogeneous
+    grid (first evaluation at eps = ebar); other points of the same batch
+    evaluate fine."""
+    p = gsm.MichelSuquetParams(E=55e9, nu=0.33, sigma_Y=25e6, H=11999049.779393503,
+                               eps0_dot=0.001761331668073649, sigma_d=116442.23751767876, n=10.0)
+    law = gsm.MichelSuquet(p)
+    ep = np.array([0.00086759, 0.00034892, -0.00137607, 0.00095601, 0.00047135, -0.000567])
+    dt = 0.43330783852286625
+    out = dict(params=np.array([p.E, p.nu, p.sigma_Y, p.H, p.eps0_dot, p.sigma_d, p.n]), eps_np1=ep, dt=np.array(dt))
+    raised = {}
+    try:
+        gsm.conventional_evaluate(law, np.zeros((1, 6)), np.zeros((1, 7)), ep[None], dt)
+        raised["conventional_evaluate"] = ""
+    except gsm.NewtonError as exc:
+        raised["conventional_evaluate"] = type(exc).__name__
+    try:
+        evaluate_arrays(law, CONV, np.zeros((1, 6)), np.zeros((1, 7)), ep[None], dt)
+        raised["evaluate_arrays"] = ""
+    except gsm.NewtonError as exc:
+        raised["evaluate_arrays"] = type(exc).__name__
+    hom = H.Homogenizer(H.VoxelGrid(np.zeros((2, 2, 2), np.uint8), [law]), CONV)
+    try:
+        hom.solve_step(ep, dt, free_mask=np.zeros(6, bool))
+        raised["solve_step"] = ""
+    except gsm.NewtonError as exc:
+        raised["solve_step"] = type(exc).__name__
+    # a smaller strain of the same law evaluates fine
+    ok = 0.01 * ep
+    sig, a_new, C = gsm.conventional_evaluate(law, np.zeros((1, 6)), np.zeros((1, 7)), ok[None], dt,
+                                              want_tangent=True)
+    out.update(ok_eps=ok, ok_sigma=sig[0], ok_a=a_new[0], ok_C=C[0])
+    for k, v in raised.items():
+        out[f"raised_{k}"] = np.array(v)
+    print("radial stall:", raised)
+    save("radial_stall.npz", **out)
+
+
 def _path_by_hand(n, cfg, name, steps, last=None):
     """The reference's run_loading_path sequence (homogenize.py:485-528) by hand."""
     t0 = time.time()
@@ -622,6 +663,7 @@ if __name__ == "__main__":
         "path8": make_path8,
         "path8_ode23": make_path8_ode23,
         "path8_ode23_fail": make_path8_ode23_fail,
+        "radial": make_radial_stall,
         "path32": lambda: make_path_conv(32),
         "path64": lambda: make_path_conv(64),
     }

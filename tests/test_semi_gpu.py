@@ -90,3 +90,32 @@ def test_conventional_rejects_linear_elastic(api):
     cfg = SC(strategy="conventional", integrator="implicit-euler")
     with pytest.raises(ConfigError):
         ev(gsm.LinearElastic(1e9, 0.3), cfg, np.zeros((2, 6)), np.zeros((2, 0)), np.zeros((2, 6)), 0.1)
+
+
+def test_radial_return_stall_raises_everywhere():
+    """A stalled radial return (gsm.py:377-378) raises gsm.NewtonError from
+    conventional_evaluate, evaluate_arrays(strategy="conventional") and the
+    basic scheme's solve_step, like the reference (fixture radial_stall.npz);
+    a smaller strain of the same law matches the reference."""
+    from paper_2006_04391_b200 import gsm
+    from paper_2006_04391_b200 import homogenize as H
+    from paper_2006_04391_b200.evaluator import StrategyConfig, evaluate_arrays
+
+    g = golden("radial_stall.npz")
+    for k in ("conventional_evaluate", "evaluate_arrays", "solve_step"):
+        assert str(g[f"raised_{k}"]) == "NewtonError"
+    law = gsm.MichelSuquet(gsm.MichelSuquetParams(*g["params"]))
+    conv = StrategyConfig(strategy="conventional", integrator="implicit-euler")
+    ep, dt = g["eps_np1"], float(g["dt"])
+    z6, z7 = np.zeros((1, 6)), np.zeros((1, 7))
+    with pytest.raises(gsm.NewtonError):
+        gsm.conventional_evaluate(law, z6, z7, ep[None], dt)
+    with pytest.raises(gsm.NewtonError):
+        evaluate_arrays(law, conv, z6, z7, ep[None], dt)
+    hom = H.Homogenizer(H.VoxelGrid(np.zeros((2, 2, 2), np.uint8), [law]), conv)
+    with pytest.raises(gsm.NewtonError):
+        hom.solve_step(ep, dt, free_mask=np.zeros(6, bool))
+    sig, a, C = gsm.conventional_evaluate(law, z6, z7, g["ok_eps"][None], dt, want_tangent=True)
+    assert_close(sig[0], g["ok_sigma"], TOL_STATE, "sigma")
+    assert_close(a[0], g["ok_a"], TOL_STATE, "a")
+    assert_close(C[0], g["ok_C"], TOL_TANGENT, "C")
