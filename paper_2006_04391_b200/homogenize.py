@@ -329,7 +329,8 @@ class Homogenizer:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib._LIB is not None:
+        lib = getattr(_lib, "_LIB", None) if _lib is not None else None  # module globals go away at shutdown
+        if h is not None and h.value and lib is not None:
             grid = getattr(self, "grid", None)
             ref = grid._solver if grid is not None else None
             if ref is not None and self.comm is None and ref() in (None, self) and getattr(self, "_state_dirty", False):
@@ -337,7 +338,7 @@ class Homogenizer:
                     self._pull_state(grid._state)
                 except Exception:  # noqa: BLE001 - best effort during teardown
                     pass
-            _lib._LIB.am_solver_destroy(h)
+            lib.am_solver_destroy(h)
             self._h = None
 
     # -- state transfer --------------------------------------------------------
