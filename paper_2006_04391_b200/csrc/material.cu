@@ -478,6 +478,15 @@ extern "C" int am_eval_batch_host(const am_law* law, const am_cfg* cfg, int64_t 
     std::lock_guard<std::mutex> lock(P.mu);
     const int64_t chunk = B < (int64_t(1) << AM_HOST_CHUNK_LOG2) ? B : (int64_t(1) << AM_HOST_CHUNK_LOG2);
     AM_TRY(P.ensure(chunk));
+    // on every return (including errors) no copy into or out of the
+    // caller's arrays is still in flight
+    struct Drain {
+        HostPipe& p;
+        ~Drain() {
+            for (int s = 0; s < HostPipe::kSlots; ++s)
+                if (p.stream[s]) cudaStreamSynchronize(p.stream[s]);
+        }
+    } drain_all{P};
     // which host arrays need staging (pageable memory)
     const double* ins[4] = {eps_n, m ? a_n : nullptr, eps_np1, dt};
     const int inw[4] = {6, m, 6, 1};                         // doubles per point
