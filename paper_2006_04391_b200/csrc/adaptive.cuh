@@ -473,6 +473,10 @@ AM_HD int adaptive_point(const Law& L, const StepCtl& ctl, const double* eps_n, 
 // The error norm gathers the column terms with shuffles and sums them in
 // the reference's (i, j) order (odeint.py:564-617).
 
+#ifndef AM_LANES_SMEM
+#define AM_LANES_SMEM 0
+#endif
+
 template <int... I>
 AM_HD auto eps_lane_tup(const double* e, double r, int j, std::integer_sequence<int, I...>) {
     auto mk = [&](int i) {
@@ -539,7 +543,7 @@ template <class Law, int Scheme>
 __device__ int adaptive_point_lanes(const Law& L, const StepCtl& ctl, const double* eps_n, const double* a_n,
                                     const double* eps_np1, double dt, double* a, double* dacol, int& substeps,
                                     int& rejected, int j, unsigned gmask, int gbase, double* rec_h,
-                                    uint8_t* rec_acc) {
+                                    uint8_t* rec_acc, double* gs = nullptr, int gst = 0) {
     using T = Tableau<Scheme>;
     constexpr int m = Law::m;
     constexpr int s = T::s;
@@ -556,14 +560,24 @@ __device__ int adaptive_point_lanes(const Law& L, const StepCtl& ctl, const doub
         if (attempts > max_attempts) return ST_INTEGRATION;  // global attempt cap
         double hi = fmin(h, dt - t);
         const bool clipped = hi >= dt - t - 1e-15 * dt;
-        double G[s][m], Gd[s][m];
+        // stage slopes: registers, or (gs) this thread's strided slice of
+        // shared memory, element (q, i) at gs[(q * m + i) * gst]
+        double Greg[AM_LANES_SMEM ? 1 : s][m], Gdreg[AM_LANES_SMEM ? 1 : s][m];
+        auto G = [&](int q, int i) -> double& {
+            if constexpr (AM_LANES_SMEM) return gs[(q * m + i) * gst];
+            else return Greg[q][i];
+        };
+        auto Gd = [&](int q, int i) -> double& {
+            if constexpr (AM_LANES_SMEM) return gs[((s + q) * m + i) * gst];
+            else return Gdreg[q][i];
+        };
         double yh[m], yl[m], dh[m], dl[m];
         bool ok = true;
         auto stage = [&](int st) {
             if (st == 0 && g1_valid) {  // FSAL reuse (odeint.py:443-453)
                 for (int i = 0; i < m; ++i) {
-                    G[0][i] = g1[i];
-                    Gd[0][i] = gd1[i];
+                    G(0, i) = g1[i];
+                    Gd(0, i) = gd1[i];
                 }
                 return;
             }
@@ -577,14 +591,19 @@ __device__ int adaptive_point_lanes(const Law& L, const StepCtl& ctl, const doub
                 if (aq == 0.0) continue;
                 const double w = hi * aq;
                 for (int i = 0; i < m; ++i) {
-                    yi[i] += w * G[q][i];
-                    ydi[i] += w * Gd[q][i];
+                    yi[i] += w * G(q, i);
+                    ydi[i] += w * Gd(q, i);
                 }
             }
             const double ti = t + T::c(st) * hi;
             double e[6];
             const double r = strain_at(eps_n, eps_np1, ti, dt, e);
-            rhs_dual_lane(L, e, r, j, yi, ydi, G[st], Gd[st]);
+            double fo[m], fco[m];
+            rhs_dual_lane(L, e, r, j, yi, ydi, fo, fco);
+            for (int i = 0; i < m; ++i) {
+                G(st, i) = fo[i];
+                Gd(st, i) = fco[i];
+            }
         };
         if constexpr (s == 2) {
             stage(0);
@@ -595,10 +614,10 @@ __device__ int adaptive_point_lanes(const Law& L, const StepCtl& ctl, const doub
         for (int i = 0; i < m; ++i) {
             double sh = 0.0, sl = 0.0, ch = 0.0, cl = 0.0;
             for (int q = 0; q < s; ++q) {
-                sh += T::b(q) * G[q][i];
-                sl += T::be(q) * G[q][i];
-                ch += T::b(q) * Gd[q][i];
-                cl += T::be(q) * Gd[q][i];
+                sh += T::b(q) * G(q, i);
+                sl += T::be(q) * G(q, i);
+                ch += T::b(q) * Gd(q, i);
+                cl += T::be(q) * Gd(q, i);
             }
             yh[i] = a[i] + hi * sh;
             yl[i] = a[i] + hi * sl;
@@ -650,8 +669,8 @@ __device__ int adaptive_point_lanes(const Law& L, const StepCtl& ctl, const doub
         if constexpr (T::fsal) {  // odeint.py:712-723
             const int src = accept ? s - 1 : 0;
             for (int i = 0; i < m; ++i) {
-                g1[i] = G[src][i];
-                gd1[i] = Gd[src][i];
+                g1[i] = G(src, i);
+                gd1[i] = Gd(src, i);
             }
             g1_valid = true;
         }

@@ -213,8 +213,13 @@ __global__ void __launch_bounds__(128, AM_LANES_MINB) k_adaptive_lanes(Law L, KA
         } else {
             double* rh = k.rec_h ? k.rec_h + k.rec_off[b] : nullptr;
             uint8_t* ra = k.rec_h ? k.rec_acc + k.rec_off[b] : nullptr;
+            double* gs = nullptr;
+            if constexpr (AM_LANES_SMEM) {
+                extern __shared__ double lanes_smem[];
+                gs = lanes_smem + threadIdx.x;  // slice of this thread, stride blockDim.x
+            }
             st = adaptive_point_lanes<Law, Scheme>(L, k.sctl, en, an, ep, dt, a, dacol, sub, rej, j, gmask, gbase, rh,
-                                                   ra);
+                                                   ra, gs, (int)blockDim.x);
             clamp_state<Law>(a, ac);  // evaluator.py:198
             // evaluator.py:200 (semi-automatic: the hand-coded tangent, gsm.py:553-560)
             if constexpr (is_semi_v<Law>) semi_stress_tangent_cols(L, ep, ac, dacol, 1, j, sig, ccol);
@@ -285,7 +290,16 @@ int launch_adaptive(const Law& L, const KArgs& k, unsigned g, cudaStream_t s) {
     if (k.C && AM_ADAPT_LANES && Scheme == 23) {
         int64_t blocks = (k.B + 19) / 20;  // 4 warps x 5 points
         if (blocks > (int64_t)kSMs * 512) blocks = (int64_t)kSMs * 512;
-        k_adaptive_lanes<Law, Scheme><<<(unsigned)blocks, 128, 0, s>>>(L, k);
+        const size_t smem = AM_LANES_SMEM ? sizeof(double) * 2 * Tableau<Scheme>::s * Law::m * 128 : 0;
+        if (smem > 48 * 1024) {
+            static bool opted = false;  // per instantiation and process (the attribute is per function)
+            if (!opted) {
+                AM_CUDA(cudaFuncSetAttribute(k_adaptive_lanes<Law, Scheme>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+                opted = true;
+            }
+        }
+        k_adaptive_lanes<Law, Scheme><<<(unsigned)blocks, 128, smem, s>>>(L, k);
     } else if (k.C) k_adaptive<Law, Scheme, true><<<g, 128, 0, s>>>(L, k);
     else k_adaptive<Law, Scheme, false><<<g, 128, 0, s>>>(L, k);
     AM_CUDA(cudaGetLastError());
