@@ -401,6 +401,8 @@ def main():
     ap.add_argument("--big-iterations", type=int, default=0,
                     help="config-5 iterations timed on one GPU (0: 300; the full load step on >1 GPU)")
     ap.add_argument("--no-strategies", action="store_true")
+    ap.add_argument("--watchdog", type=float, default=1500.0,
+                    help="seconds allowed for the basic-scheme runs before the line is printed with an error")
     ap.add_argument("--p2p", action="store_true",
                     help="at >1 GPU also time config 4 with the fused P2P (CUDA IPC) transposes")
     args = ap.parse_args()
@@ -611,11 +613,76 @@ def main():
     del d_en, d_an, d_ep, d_dt, d_sig, d_a, d_C, d_it, d_st
     torch.cuda.empty_cache()
 
+    basic, errors = {}, []
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config 2: {B} EVP material points per GPU, stress + second-order AD tangent",
+                   "law": "MichelSuquet(ALUMINUM_MATRIX)", "strategy": "automatic", "integrator": "implicit-euler",
+                   "batch_per_gpu": B, "parallelism": f"dp{world} (independent points, no collective)",
+                   "l2": "inputs+outputs 552 MiB per step > 126 MB L2 (no flush needed)",
+                   "mean_newton_iters": float(iters.mean())},
+        "roofline": {"bound": "fp64", "kernel": "k_material<MichelSuquetLaw> (Newton, the dominant kernel)",
+                     "achieved": fl_newton / (t_newton * 1e-3) / 1e12, "peak": peak.value, "unit": "TFLOP/s",
+                     "frac": fl_newton / (t_newton * 1e-3) / 1e12 / peak.value if peak.value else None,
+                     "traffic": traffic_newton,
+                     "traffic_source": "ncu dram__bytes_read + dram__bytes_write of this kernel per point "
+                                       "(profiles/r02/traffic.json) x points per launch",
+                     "peak_source": "measured: am_probe_fp64_tflops DFMA microbenchmark on this GPU "
+                                    "(MEASURED_PEAKS.json has no fp64 entry)",
+                     "work_per_launch": f"{fl_newton:.4g} algorithmic fp64 flops per launch (1072 per Newton "
+                                        "iteration of each point + 18, SURVEY §8d)",
+                     "launch_ms": t_newton, "share_of_step": t_newton / (t_newton + t_tangent),
+                     "timing": "CUDA events around each kernel on the launching stream (am_k1_timing), "
+                               f"{int(kt[2])} launches",
+                     "tangent_kernel": {"kernel": "k_tangent<MichelSuquetLaw>", "launch_ms": t_tangent,
+                                        "achieved": fl_tangent / (t_tangent * 1e-3) / 1e12,
+                                        "frac": fl_tangent / (t_tangent * 1e-3) / 1e12 / peak.value,
+                                        "work_per_launch": f"{fl_tangent:.4g} flops (2255 per point)",
+                                        "traffic": traffic_tangent},
+                     "step": {"achieved": achieved, "frac": achieved / peak.value if peak.value else None,
+                              "traffic": traffic,
+                              "work_per_step": f"{fl:.4g} flops (1072*N_it + 2273 per eval); one step = the "
+                                               "Newton kernel + the tangent kernel"}},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "evaluator.evaluate_arrays (the reference's drop-in call) with the caller's pageable numpy "
+                        "arrays -> am_eval_batch_host: pinned staging of the inputs by a host copy pool, results "
+                        "returned in pooled page-locked numpy arrays, 3-stream chunked H2D|kernels|D2H",
+                "c_abi_pinned": {"value": abi_value, "unit": UNIT,
+                                 "path": "am_eval_batch_host (C ABI) with caller-pinned host AoS buffers"},
+                "pcie_ceiling": pcie_ceiling, "frac_of_pcie_ceiling": e2e_value / world / pcie_ceiling,
+                "pcie_ceiling_note": "same bytes as concurrent pinned H2D + D2H copies without kernels (per GPU)"},
+        "gpu_launches": 2 * args.steps,
+        "gpu_launches_note": "K1 launches (Newton + tangent kernel) of the config-2 timed region",
+        "clocks": clocks,
+        "basic_scheme": basic,
+    }
+    if strategies:
+        line["strategies"] = strategies
+        line["strategies_note"] = ("config-2 batch, stress + tangent, device-resident, 5 launches each after 2 "
+                                   "warm-up; conventional = the paper's hand-derived radial return baseline")
+    # a hang in a collective must not swallow the headline: past the budget
+    # rank 0 prints the line with an error key and every rank exits non-zero
+    import threading
+
+    current = {"key": None}
+
+    def watchdog():
+        if rank == 0:
+            line["error"] = (f"watchdog: basic-scheme runs exceeded {args.watchdog} s "
+                             f"(in {current['key']})")
+            print(json.dumps(line), flush=True)
+        os._exit(3)
+
+    dog = threading.Timer(args.watchdog, watchdog)
+    dog.daemon = True
+    dog.start()
+
     # ---- basic scheme (configs 1, 3, 4, 5): first-class keys; a failure
     # fails the bench (non-zero exit after the line)
     from paper_2006_04391_b200 import distributed as D, homogenize as H
 
-    basic, errors = {}, []
     comm_of = (lambda transport: D.comm_from_torch(transport=transport)) if dist is not None else (lambda t: None)
     par = (lambda t: "single GPU (3-D cuFFT)" if world == 1 else
            f"x-slabs over {world} GPUs, 2-D cuFFT + {'ncclAlltoAll' if t == 'nccl' else 'fused P2P pack/unpack over NVLink'}"
@@ -625,6 +692,7 @@ def main():
                  "basic-scheme iterations)")
 
     def guarded(key, fn):
+        current["key"] = key
         try:
             basic[key] = fn()
         except Exception as exc:  # noqa: BLE001 - reported, then the bench exits non-zero
@@ -726,6 +794,7 @@ def main():
 
         guarded("config4_step1_slab_algorithm", slab_alg)
 
+    dog.cancel()
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -733,54 +802,6 @@ def main():
             sys.exit(1)
         return
 
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config 2: {B} EVP material points per GPU, stress + second-order AD tangent",
-                   "law": "MichelSuquet(ALUMINUM_MATRIX)", "strategy": "automatic", "integrator": "implicit-euler",
-                   "batch_per_gpu": B, "parallelism": f"dp{world} (independent points, no collective)",
-                   "l2": "inputs+outputs 552 MiB per step > 126 MB L2 (no flush needed)",
-                   "mean_newton_iters": float(iters.mean())},
-        "roofline": {"bound": "fp64", "kernel": "k_material<MichelSuquetLaw> (Newton, the dominant kernel)",
-                     "achieved": fl_newton / (t_newton * 1e-3) / 1e12, "peak": peak.value, "unit": "TFLOP/s",
-                     "frac": fl_newton / (t_newton * 1e-3) / 1e12 / peak.value if peak.value else None,
-                     "traffic": traffic_newton,
-                     "traffic_source": "ncu dram__bytes_read + dram__bytes_write of this kernel per point "
-                                       "(profiles/r02/traffic.json) x points per launch",
-                     "peak_source": "measured: am_probe_fp64_tflops DFMA microbenchmark on this GPU "
-                                    "(MEASURED_PEAKS.json has no fp64 entry)",
-                     "work_per_launch": f"{fl_newton:.4g} algorithmic fp64 flops per launch (1072 per Newton "
-                                        "iteration of each point + 18, SURVEY §8d)",
-                     "launch_ms": t_newton, "share_of_step": t_newton / (t_newton + t_tangent),
-                     "timing": "CUDA events around each kernel on the launching stream (am_k1_timing), "
-                               f"{int(kt[2])} launches",
-                     "tangent_kernel": {"kernel": "k_tangent<MichelSuquetLaw>", "launch_ms": t_tangent,
-                                        "achieved": fl_tangent / (t_tangent * 1e-3) / 1e12,
-                                        "frac": fl_tangent / (t_tangent * 1e-3) / 1e12 / peak.value,
-                                        "work_per_launch": f"{fl_tangent:.4g} flops (2255 per point)",
-                                        "traffic": traffic_tangent},
-                     "step": {"achieved": achieved, "frac": achieved / peak.value if peak.value else None,
-                              "traffic": traffic,
-                              "work_per_step": f"{fl:.4g} flops (1072*N_it + 2273 per eval); one step = the "
-                                               "Newton kernel + the tangent kernel"}},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "evaluator.evaluate_arrays (the reference's drop-in call) with the caller's pageable numpy "
-                        "arrays -> am_eval_batch_host: pinned staging of the inputs by a host copy pool, results "
-                        "returned in pooled page-locked numpy arrays, 3-stream chunked H2D|kernels|D2H",
-                "c_abi_pinned": {"value": abi_value, "unit": UNIT,
-                                 "path": "am_eval_batch_host (C ABI) with caller-pinned host AoS buffers"},
-                "pcie_ceiling": pcie_ceiling, "frac_of_pcie_ceiling": e2e_value / world / pcie_ceiling,
-                "pcie_ceiling_note": "same bytes as concurrent pinned H2D + D2H copies without kernels (per GPU)"},
-        "gpu_launches": 2 * args.steps,
-        "gpu_launches_note": "K1 launches (Newton + tangent kernel) of the config-2 timed region",
-        "clocks": clocks,
-        "basic_scheme": basic,
-    }
-    if strategies:
-        line["strategies"] = strategies
-        line["strategies_note"] = ("config-2 batch, stress + tangent, device-resident, 5 launches each after 2 "
-                                   "warm-up; conventional = the paper's hand-derived radial return baseline")
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
         if args.basic or args.path:
