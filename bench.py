@@ -802,7 +802,7 @@ def main():
             sys.exit(1)
         return
 
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the CPU arm is timed at N = 1 only
         line["cpu_baseline"] = cpu_baseline()
         if args.basic or args.path:
             threads = os.cpu_count() or 1
