@@ -390,3 +390,30 @@ def test_grid_keeps_committed_state(H, AUTO):
     committed = [a.copy() for a in g8.state]
     del hom  # released: the grid keeps what was committed
     assert rel(g8.state[0], committed[0]) == 0.0
+
+
+def test_graph_replay_bitwise_equal_to_eager(H, AUTO):
+    """The per-step CUDA graph replays the eager iteration's kernels in the
+    same order: fields and histories are bitwise identical (AM_NO_GRAPHS=1
+    selects the eager path at solver creation)."""
+    import os
+
+    out = []
+    for off in ("1", "0"):
+        os.environ["AM_NO_GRAPHS"] = off
+        try:
+            hom = H.Homogenizer(H.toy_mmc_grid(16), AUTO)
+        finally:
+            os.environ.pop("AM_NO_GRAPHS", None)
+        path = H.LoadingPath(steps=20)
+        t = path.times()
+        res = []
+        for k in (1, 2):
+            eb = np.zeros(6)
+            eb[0] = path.eps_xx(t[k])
+            eps, sig, info = hom.solve_step(eb, t[k] - t[k - 1], free_mask=np.array([False] + [True] * 5))
+            res.append((eps, sig, info.history))
+            hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+        out.append(res)
+    for (e0, s0, h0), (e1, s1, h1) in zip(*out):
+        assert np.array_equal(e0, e1) and np.array_equal(s0, s1) and h0 == h1
