@@ -117,6 +117,9 @@ __global__ void k_shift(double* __restrict__ eps, const double* __restrict__ eps
 #ifndef AM_FOURIER_MINB
 #define AM_FOURIER_MINB 1
 #endif
+#ifndef AM_FOURIER_EARLY
+#define AM_FOURIER_EARLY 1
+#endif
 __global__ void __launch_bounds__(kRedThreads, AM_FOURIER_MINB) k_fourier(Spec sp, RefMat ref, double2* __restrict__ S,
                                                          double2* __restrict__ ehat, double* __restrict__ red,
                                                          int update) {
@@ -132,19 +135,105 @@ __global__ void __launch_bounds__(kRedThreads, AM_FOURIER_MINB) k_fourier(Spec s
         const int64_t q = kx * sp.xs + (int64_t)kyl * sp.nzh + kz;
         const Bin b = make_bin(kx, ky, kz, sp.nx, sp.ny, sp.nz);
         cplx s[6];
+#if AM_FOURIER_EARLY
+        // both spectra's loads in flight together (one memory latency per bin)
+        double2 ev[6];
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
             const double2 v = S[c * sp.cs + q];
             s[c] = cplx{v.x, v.y};
+            ev[c] = update ? ehat[c * sp.cs + q] : make_double2(0.0, 0.0);
+        }
+#else
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            const double2 v = S[c * sp.cs + q];
+            s[c] = cplx{v.x, v.y};
+        }
+#endif
+        if (!b.zero) acc += rfft_weight(kz, sp.nz) * traction_sq(b, s);
+        if (update && !b.zero) {
+            double er[6], ei[6], cr[6], ci[6], tr[6], ti[6], outr[6], outi[6];
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+#if AM_FOURIER_EARLY
+                const double2 v = ev[c];
+#else
+                const double2 v = ehat[c * sp.cs + q];
+#endif
+                er[c] = v.x;
+                ei[c] = v.y;
+            }
+            iso_apply(ref, er, cr);
+            iso_apply(ref, ei, ci);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                tr[c] = s[c].re - cr[c];
+                ti[c] = s[c].im - ci[c];
+            }
+            green_apply_real(ref, b, tr, outr);
+            green_apply_real(ref, b, ti, outi);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                ehat[c * sp.cs + q] = make_double2(outr[c], outi[c]);
+                S[c * sp.cs + q] = make_double2(outr[c] * invN, outi[c] * invN);
+            }
+        }
+    }
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) red[(int64_t)ky * kParts + part] = t;
+}
+
+// k_fourier with the next bin's spectra loaded before the current bin's
+// results are stored (software pipelining; AM_FOURIER_PF=1)
+__global__ void __launch_bounds__(kRedThreads, AM_FOURIER_MINB) k_fourier_pf(Spec sp, RefMat ref, double2* __restrict__ S,
+                                                            double2* __restrict__ ehat, double* __restrict__ red,
+                                                            int update) {
+    __shared__ double sh[kRedThreads / 32];
+    const int kyl = blockIdx.x / kParts, part = blockIdx.x % kParts;
+    const int ky = sp.y0 + kyl;
+    const int64_t nb = (int64_t)sp.nx * sp.nzh;
+    const int64_t lo = nb * part / kParts, hi = nb * (part + 1) / kParts;
+    const double invN = 1.0 / (double)sp.N;
+    double acc = 0.0;
+    auto qof = [&](int64_t j) { return (int64_t)(j / sp.nzh) * sp.xs + (int64_t)kyl * sp.nzh + (int)(j % sp.nzh); };
+    double2 sv[6], ev[6];
+    int64_t j = lo + threadIdx.x;
+    if (j < hi) {
+        const int64_t q = qof(j);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            sv[c] = S[c * sp.cs + q];
+            ev[c] = update ? ehat[c * sp.cs + q] : make_double2(0.0, 0.0);
+        }
+    }
+    for (; j < hi; j += blockDim.x) {
+        const int kx = (int)(j / sp.nzh), kz = (int)(j % sp.nzh);
+        const int64_t q = kx * sp.xs + (int64_t)kyl * sp.nzh + kz;
+        const Bin b = make_bin(kx, ky, kz, sp.nx, sp.ny, sp.nz);
+        cplx s[6];
+        double2 e[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            s[c] = cplx{sv[c].x, sv[c].y};
+            e[c] = ev[c];
+        }
+        const int64_t jn = j + blockDim.x;
+        if (jn < hi) {  // the next bin's loads in flight during this bin's work
+            const int64_t qn = qof(jn);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                sv[c] = S[c * sp.cs + qn];
+                ev[c] = update ? ehat[c * sp.cs + qn] : make_double2(0.0, 0.0);
+            }
         }
         if (!b.zero) acc += rfft_weight(kz, sp.nz) * traction_sq(b, s);
         if (update && !b.zero) {
             double er[6], ei[6], cr[6], ci[6], tr[6], ti[6], outr[6], outi[6];
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
-                const double2 v = ehat[c * sp.cs + q];
-                er[c] = v.x;
-                ei[c] = v.y;
+                er[c] = e[c].x;
+                ei[c] = e[c].y;
             }
             iso_apply(ref, er, cr);
             iso_apply(ref, ei, ci);
@@ -744,7 +833,13 @@ static int fourier_enqueue(am_solver* h, bool update) {
     for (size_t i = 0; i < h->slabs.size(); ++i) {
         Slab& s = h->slabs[i];
         double* red = h->red + (int64_t)i * L;
-        k_fourier<<<s.sp.nyl * kParts, kRedThreads, 0, h->stream>>>(s.sp, ref, s.S, s.ehat, red, update ? 1 : 0);
+#ifndef AM_FOURIER_PF
+#define AM_FOURIER_PF 0
+#endif
+        if (AM_FOURIER_PF)
+            k_fourier_pf<<<s.sp.nyl * kParts, kRedThreads, 0, h->stream>>>(s.sp, ref, s.S, s.ehat, red, update ? 1 : 0);
+        else
+            k_fourier<<<s.sp.nyl * kParts, kRedThreads, 0, h->stream>>>(s.sp, ref, s.S, s.ehat, red, update ? 1 : 0);
         AM_CUDA(cudaGetLastError());
         k_finish<<<1, 32, 0, h->stream>>>(s.S, s.sp.cs, s.y0 == 0 ? 1 : 0, s.flags, s.subs, red,
                                           (int64_t)h->ny * kParts);
