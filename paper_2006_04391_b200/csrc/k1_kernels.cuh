@@ -57,6 +57,11 @@ struct PointIO {
         eo = g * k.le.es;
         ao = b * k.la.es;
     }
+    // with the gather index already loaded (prefetched by the caller)
+    __device__ PointIO(const KArgs& k_, int64_t b_, int64_t g) : k(k_), b(b_) {
+        eo = g * k.le.es;
+        ao = b * k.la.es;
+    }
     __device__ void eps(double* en, double* ep) const {
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
@@ -85,12 +90,37 @@ struct PointIO {
     }
 };
 
+#ifndef AM_GS_WAVES
+#define AM_GS_WAVES 16
+#endif
+#ifndef AM_GS_PREFETCH
+#define AM_GS_PREFETCH 0
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 template <class Law, int Mode, bool Raw>
 __global__ void __launch_bounds__(128, AM_K1_MINB_N) k_material(Law L, KArgs k) {
     constexpr int m = Law::m;
     constexpr int ms = m > 0 ? m : 1;
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
-        const PointIO io(k, b);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // gathered (solver) launches: the next point's gather index is loaded
+    // while this point is evaluated (one dependent-load latency fewer)
+    int64_t gnext = (k.gidx && b < k.B) ? k.gidx[b] : b;
+    for (; b < k.B; b += stride) {
+        const int64_t g = gnext;
+        if (k.gidx && b + stride < k.B) {
+            gnext = k.gidx[b + stride];
+            if (AM_GS_PREFETCH) {  // the next point's inputs into L2 (no registers held)
+#pragma unroll
+                for (int c = 0; c < 6; ++c) {
+                    prefetch_l2(k.eps_n + c * k.le.cs + gnext * k.le.es);
+                    prefetch_l2(k.eps_np1 + c * k.le.cs + gnext * k.le.es);
+                }
+#pragma unroll
+                for (int c = 0; c < m; ++c) prefetch_l2(k.a_n + c * k.la.cs + (b + stride) * k.la.es);
+            }
+        }
+        const PointIO io(k, b, k.gidx ? g : b);
         double en[6], ep[6], an[ms], a[ms];
         io.eps(en, ep);
         io.load_a<m>(k.a_n, an);
@@ -323,8 +353,11 @@ int launch_law(const Law& L, KArgs k, cudaStream_t s) {
             return launch_adaptive_law(L, k, g, s);  // k1_adapt_*.cu
     }
     if (!k.C) {
-        if (stress) k_material<Law, 1, false><<<g, threads, 0, s>>>(L, k);
-        else k_material<Law, 0, false><<<g, threads, 0, s>>>(L, k);
+        unsigned gg = g;
+        if (AM_GS_WAVES && k.gidx && gg > (unsigned)(kSMs * AM_K1_MINB_N * AM_GS_WAVES))
+            gg = (unsigned)(kSMs * AM_K1_MINB_N * AM_GS_WAVES);  // grid-stride: the gidx prefetch pays
+        if (stress) k_material<Law, 1, false><<<gg, threads, 0, s>>>(L, k);
+        else k_material<Law, 0, false><<<gg, threads, 0, s>>>(L, k);
         AM_CUDA(cudaGetLastError());
         return AM_OK;
     }
