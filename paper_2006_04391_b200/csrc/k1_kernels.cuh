@@ -96,6 +96,12 @@ struct PointIO {
 #ifndef AM_GS_PREFETCH
 #define AM_GS_PREFETCH 0
 #endif
+#ifndef AM_TAN_WAVES
+#define AM_TAN_WAVES 0
+#endif
+#ifndef AM_TAN_PREFETCH
+#define AM_TAN_PREFETCH 0
+#endif
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 template <class Law, int Mode, bool Raw>
 __global__ void __launch_bounds__(128, AM_K1_MINB_N) k_material(Law L, KArgs k) {
@@ -148,7 +154,19 @@ template <class Law>
 __global__ void __launch_bounds__(128, AM_K1_MINB_T) k_tangent(Law L, KArgs k) {
     constexpr int m = Law::m;
     constexpr int ms = m > 0 ? m : 1;
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < k.B; b += stride) {
+        if (AM_TAN_PREFETCH && b + stride < k.B) {  // the next point's inputs into L2
+            const int64_t bn = b + stride;
+            const int64_t gn = k.gidx ? k.gidx[bn] : bn;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                prefetch_l2(k.eps_n + c * k.le.cs + gn * k.le.es);
+                prefetch_l2(k.eps_np1 + c * k.le.cs + gn * k.le.es);
+            }
+#pragma unroll
+            for (int c = 0; c < m; ++c) prefetch_l2(k.a_out + c * k.la.cs + bn * k.la.es);
+        }
         const PointIO io(k, b);
         double en[6], ep[6], a[ms], ac[ms], sig[6];
         io.eps(en, ep);
@@ -379,7 +397,9 @@ int launch_law(const Law& L, KArgs k, cudaStream_t s) {
         AM_CUDA(cudaGetLastError());
     }
     k1_mark(1, s);
-    k_tangent<Law><<<g, threads, 0, s>>>(L, k);
+    unsigned gt = g;
+    if (AM_TAN_WAVES && gt > (unsigned)(kSMs * 2 * AM_TAN_WAVES)) gt = (unsigned)(kSMs * 2 * AM_TAN_WAVES);
+    k_tangent<Law><<<gt, threads, 0, s>>>(L, k);
     AM_CUDA(cudaGetLastError());
     k1_mark(2, s);
     if (scratch) AM_CUDA(cudaFreeAsync(scratch, s));
