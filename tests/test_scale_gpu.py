@@ -156,3 +156,33 @@ def test_config5_512_step1(mods, parity_log):
     _sampled_voxels(mods, grid, hom, eps, sig, dt, 1 << 16, parity_log, "config5_512_sampled")
     del hom, eps, sig
     _field_step(mods, grid, dt, eb, 20, parity_log, "config5_512_field_step", slabwise=True)
+
+
+def test_config4_256_slab_algorithm(mods, parity_log):
+    """The multi-GPU algorithm (x slabs, 2-D FFTs, transposes, 1-D FFTs over
+    x) at the config-4 size, on 2 / 4 / 8 slabs of one GPU: the single-slab
+    run's iteration count, fields within 1e-10, and bitwise equal results
+    for every slab count (the NCCL mode runs the same kernels per rank)."""
+    _, H, cfg, _ = mods
+    grid = _grid(mods, 256, None)
+    eb, dt = _step1(H)
+    hom = H.Homogenizer(H.VoxelGrid(grid.material_ids, grid.materials), cfg)
+    eps0, sig0, info0 = hom.solve_step(eb, dt, free_mask=FREE)
+    del hom
+    ref = None
+    errs = {}
+    for k in (2, 4, 8):
+        hom = H.Homogenizer(H.VoxelGrid(grid.material_ids, grid.materials), cfg, slabs=k)
+        eps, sig, info = hom.solve_step(eb, dt, free_mask=FREE)
+        del hom
+        assert info.iterations == info0.iterations
+        errs[f"slabs{k}_sigma"] = rel(sig, sig0)
+        errs[f"slabs{k}_eps"] = rel(eps, eps0)
+        assert errs[f"slabs{k}_sigma"] <= 1e-10 and errs[f"slabs{k}_eps"] <= 1e-10
+        if ref is None:
+            ref = (eps, sig, info.history)
+        else:
+            errs[f"slabs{k}_bitwise_equal_to_2"] = bool(np.array_equal(eps, ref[0]) and np.array_equal(sig, ref[1])
+                                                        and info.history == ref[2])
+            assert errs[f"slabs{k}_bitwise_equal_to_2"]
+    parity_log("config4_256_slab_algorithm", iterations=info0.iterations, **errs)
