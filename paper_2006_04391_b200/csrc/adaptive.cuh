@@ -526,6 +526,127 @@ __device__ __forceinline__ void stress_dual_lane(const Law& L, const double* e, 
     else run(plain_tup<Law::m>(a, seq<Law::m>{}));
 }
 
+// jac_dir2 (odeint.py:306-337) for outer direction j only (lane groups)
+template <class Law>
+__device__ __forceinline__ void jac_dir2_lane(const Law& L, const double* eps_n, const double* eps_np1, double t,
+                                              double dt, const double* y, const double* dacol, const double* v_a,
+                                              double v_t, int j, double* out) {
+    constexpr int m = Law::m;
+    double r = t / dt;
+    r = r < 1.0 ? r : 1.0;
+    D2T<1> pe[6], pa[m];
+    for (int i = 0; i < 6; ++i) {
+        const double de = eps_np1[i] - eps_n[i];
+        pe[i].v = eps_n[i] + r * de;
+        pe[i].d1 = de / dt * v_t;
+        pe[i].d2[0] = i == j ? r : 0.0;
+        pe[i].d12[0] = i == j ? v_t / dt : 0.0;
+    }
+    for (int i = 0; i < m; ++i) {
+        pa[i].v = y[i];
+        pa[i].d1 = v_a[i];
+        pa[i].d2[0] = dacol[i];
+        pa[i].d12[0] = 0.0;
+    }
+    auto f = rhs_sweep(L, tup(pe[0], pe[1], pe[2], pe[3], pe[4], pe[5]),
+                       tup(pa[0], pa[1], pa[2], pa[3], pa[4], pa[5], pa[6]));
+    sfor<m>([&](auto I) { out[decltype(I)::value] = get<decltype(I)::value>(f).d12[0]; });
+}
+
+// rosenbrock_attempt<Law, true> for sensitivity column j (lane groups): the
+// primal stages are computed identically by every lane
+template <class Law>
+__device__ bool rosenbrock_attempt_lane(const Law& L, const double* eps_n, const double* eps_np1, double dt,
+                                        double t, double h, const double* y, const double* dacol, int j, double* yh,
+                                        double* yl, double* dh, double* dl) {
+    static_assert(is_semi_v<Law>, "ode23s needs the hand-coded partials");
+    using T = Tableau<32>;
+    constexpr int m = Law::m;
+    constexpr int s = T::s;
+    double e0[6];
+    strain_at(eps_n, eps_np1, t, dt, e0);
+    double f0[m], J6[m][6], Je[m][6], J[m][m], ft[m], W[m][m];
+    int piv[m];
+    L.rhs_jac(e0, y, f0, J6, Je);
+    for (int i = 0; i < m; ++i) {
+        for (int k = 0; k < 6; ++k) J[i][k] = J6[i][k];
+        J[i][6] = 0.0;
+        double sft = 0.0;
+        for (int k = 0; k < 6; ++k) sft += Je[i][k] * ((eps_np1[k] - eps_n[k]) / dt);
+        ft[i] = sft;
+    }
+    const double g00h = T::gam(0, 0) * h;
+    for (int i = 0; i < m; ++i)
+        for (int k = 0; k < m; ++k) W[i][k] = (i == k ? 1.0 : 0.0) - g00h * J[i][k];
+    bool ok = lu_factor(W, piv);
+    double K[s][m], Kd[s][m];
+    for (int st = 0; st < s; ++st) {
+        double yi[m], ydi[m], fi[m], fdi[m];
+        for (int i = 0; i < m; ++i) {
+            yi[i] = y[i];
+            ydi[i] = dacol[i];
+        }
+        for (int q = 0; q < st; ++q)
+            if (T::a(st, q) != 0.0)
+                for (int i = 0; i < m; ++i) {
+                    yi[i] += T::a(st, q) * K[q][i];
+                    ydi[i] += T::a(st, q) * Kd[q][i];
+                }
+        const double ti = t + T::c(st) * h;
+        double e[6];
+        const double r = strain_at(eps_n, eps_np1, ti, dt, e);
+        rhs_dual_lane(L, e, r, j, yi, ydi, fi, fdi);
+        double rhs[m];
+        const double gt = h * T::gbar(st) * h;
+        for (int i = 0; i < m; ++i) rhs[i] = h * fi[i] + gt * ft[i];
+        for (int q = 0; q < st; ++q) {
+            const double g = T::gam(st, q);
+            if (g == 0.0) continue;
+            for (int i = 0; i < m; ++i) {
+                double jk = 0.0;
+                for (int n = 0; n < m; ++n) jk += J[i][n] * K[q][n];
+                rhs[i] += g * h * jk;
+            }
+        }
+        for (int i = 0; i < m; ++i) K[st][i] = ok ? rhs[i] : 0.0;
+        lu_solve(W, piv, K[st]);
+        double v_a[m], jtv[m], col[m];
+        for (int i = 0; i < m; ++i) v_a[i] = 0.0;
+        for (int q = 0; q <= st; ++q)
+            if (T::gam(st, q) != 0.0)
+                for (int i = 0; i < m; ++i) v_a[i] += T::gam(st, q) * K[q][i];
+        jac_dir2_lane(L, eps_n, eps_np1, t, dt, y, dacol, v_a, T::gbar(st) * h, j, jtv);
+        for (int i = 0; i < m; ++i) col[i] = h * fdi[i] + h * jtv[i];
+        for (int q = 0; q < st; ++q) {
+            const double g = T::gam(st, q);
+            if (g == 0.0) continue;
+            for (int i = 0; i < m; ++i) {
+                double jk = 0.0;
+                for (int n = 0; n < m; ++n) jk += J[i][n] * Kd[q][n];
+                col[i] += g * h * jk;
+            }
+        }
+        for (int i = 0; i < m; ++i) col[i] = ok ? col[i] : 0.0;
+        lu_solve(W, piv, col);
+        for (int i = 0; i < m; ++i) Kd[st][i] = col[i];
+    }
+    for (int i = 0; i < m; ++i) {
+        double sh = 0.0, sl = 0.0, ch = 0.0, cl = 0.0;
+        for (int q = 0; q < s; ++q) {
+            sh += T::b(q) * K[q][i];
+            sl += T::be(q) * K[q][i];
+            ch += T::b(q) * Kd[q][i];
+            cl += T::be(q) * Kd[q][i];
+        }
+        yh[i] = y[i] + sh;
+        yl[i] = y[i] + sl;
+        ok = ok && (yh[i] - yh[i] == 0.0) && (yl[i] - yl[i] == 0.0);
+        dh[i] = dacol[i] + ch;
+        dl[i] = dacol[i] + cl;
+    }
+    return ok;
+}
+
 // sum over (i, jj) in the reference's order of the group's per-column terms t[i]
 template <int N>
 __device__ __forceinline__ double group_sum(const double* t, unsigned gmask, int gbase) {
@@ -573,6 +694,9 @@ __device__ int adaptive_point_lanes(const Law& L, const StepCtl& ctl, const doub
         };
         double yh[m], yl[m], dh[m], dl[m];
         bool ok = true;
+        if constexpr (Scheme == 32) {
+            ok = rosenbrock_attempt_lane<Law>(L, eps_n, eps_np1, dt, t, hi, a, dacol, j, yh, yl, dh, dl);
+        } else {
         auto stage = [&](int st) {
             if (st == 0 && g1_valid) {  // FSAL reuse (odeint.py:443-453)
                 for (int i = 0; i < m; ++i) {
@@ -625,6 +749,7 @@ __device__ int adaptive_point_lanes(const Law& L, const StepCtl& ctl, const doub
             dh[i] = dacol[i] + hi * ch;
             dl[i] = dacol[i] + hi * cl;
         }
+        }  // explicit stages
         // error_norm (odeint.py:564-617)
         double total;
         int count;

@@ -330,12 +330,15 @@ __global__ void __launch_bounds__(128) k_conventional(SemiLaw<MichelSuquetLaw> S
 #ifndef AM_ADAPT_LANES
 #define AM_ADAPT_LANES 1
 #endif
+#ifndef AM_LANES_ROS
+#define AM_LANES_ROS 0
+#endif
 template <class Law, int Scheme>
 int launch_adaptive(const Law& L, const KArgs& k, unsigned g, cudaStream_t s) {
     // lane groups for ode23 (automatic): 26.3 vs 21.0 M evals/s (internal
     // measure), 12.9 vs 8.6 (stress); ode12's unrolled one-thread kernel
     // stays faster (12.3 vs 7.1) -- k1_variants.log, round 2
-    if (k.C && AM_ADAPT_LANES && Scheme == 23) {
+    if (k.C && AM_ADAPT_LANES && (Scheme == 23 || (Scheme == 32 && AM_LANES_ROS))) {
         int64_t blocks = (k.B + 19) / 20;  // 4 warps x 5 points
         if (blocks > (int64_t)kSMs * 512) blocks = (int64_t)kSMs * 512;
         const size_t smem = AM_LANES_SMEM ? sizeof(double) * 2 * Tableau<Scheme>::s * Law::m * 128 : 0;

@@ -31,8 +31,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "--one":
     d_it = torch.empty(B, dtype=torch.int32, device=dev)
     sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     out = {}
-    for integ, meas in (("ode23", "internal"), ("ode12", "internal"), ("ode23", "stress")):
-        cfg = _lib.make_cfg(StrategyConfig(integrator=integ, error_measure=meas))
+    for integ, meas, strat in (("ode23", "internal", "automatic"), ("ode12", "internal", "automatic"),
+                               ("ode23", "stress", "automatic"), ("ode23s", "internal", "semi-automatic"),
+                               ("ode23s", "stress", "semi-automatic")):
+        cfg = _lib.make_cfg(StrategyConfig(strategy=strat, integrator=integ, error_measure=meas))
 
         def run():
             _lib.check(lib.am_eval_batch(law, cfg, B, d_en.data_ptr(), d_an.data_ptr(), d_ep.data_ptr(), None, 0.05, 1,
@@ -48,7 +50,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--one":
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 3
-        out[f"{integ}/{meas}"] = f"{B / ms / 1e3:.3g} M/s ({ms:.2f} ms, substeps {d_it.double().mean().item():.2f})"
+        out[f"{strat[:4]}/{integ}/{meas}"] = f"{B / ms / 1e3:.3g} M/s ({ms:.2f} ms, substeps {d_it.double().mean().item():.2f})"
     print(os.path.basename(os.path.dirname(sys.argv[2])), out, flush=True)
 else:
     B = sys.argv[1] if len(sys.argv) > 1 else str(1 << 18)
