@@ -78,3 +78,17 @@ def conventional(law, eps_np1, a_n, dt, want_tangent):
     code = lib().hostcheck_conventional(_p(prm), ctypes.c_int64(B), _p(eps_np1), _p(an), _p(dt), int(bool(want_tangent)),
                                         _p(sig), _p(a), _p(C))
     return dict(sigma=sig, a=a, C=C if want_tangent else None, code=code)
+
+
+def tangent_point(law, eps_n, a, eps_np1, dt):
+    """Host build of the tangent post-process at a given state (no Newton)."""
+    _, prm = law
+    eps_n = np.ascontiguousarray(eps_n, dtype=float)
+    eps_np1 = np.ascontiguousarray(eps_np1, dtype=float)
+    a = np.ascontiguousarray(a, dtype=float)
+    B = eps_np1.shape[0]
+    dt = np.ascontiguousarray(np.broadcast_to(np.asarray(dt, dtype=float), (B,)))
+    sig = np.zeros((B, 6)); C = np.zeros((B, 6, 6)); st = np.zeros(B, np.uint8)
+    lib().hostcheck_tangent_point(_p(prm), ctypes.c_int64(B), _p(eps_n), _p(a), _p(eps_np1), _p(dt), _p(sig), _p(C),
+                                  st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+    return dict(sigma=sig, C=C, status=st)

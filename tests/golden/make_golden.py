@@ -553,6 +553,39 @@ def make_path8_ode23_fail():
     save("path8_ode23_fail.npz", **out)
 
 
+def make_tangent_singular():
+    """The tangent post-process's check_singular LU (odeint.py:417-426,
+    linalg.py:103-104) at given states: M = I - h df/da(eps(t1), a) for
+    plastic states and h over 1e-2 .. 1e16, with the reference's verdict
+    (SingularMatrixError or not).  In a full evaluation the Newton fails
+    first (same criterion on the iterates' M); this pins the tangent's own
+    route."""
+    law = gsm.MichelSuquet()
+    ops = gsm.LawOps(law, "automatic")
+    rng = np.random.default_rng(31)
+    B = 96
+    eps_n = rng.normal(0, 1e-3, (B, 6))
+    eps_np1 = eps_n + rng.normal(0, 1.0, (B, 6)) * 10.0 ** rng.uniform(-3, 0, (B, 1))
+    a = np.zeros((B, 7))
+    a[:, :6] = rng.normal(0, 5e-4, (B, 6))
+    a[:, 6] = np.abs(rng.normal(0, 1e-3, B))
+    dt = 10.0 ** np.linspace(-2, 16, B)
+    e1 = eps_n + 1.0 * (eps_np1 - eps_n)  # odeint.py:256-264 at t1 = h
+    _, J, _ = ops.rhs_and_jacobians(e1, a)
+    singular = np.zeros(B, dtype=bool)
+    ratio = np.zeros(B)  # min |pivot| / max|M| of the reference's LU (threshold 1e-14)
+    for b in range(B):
+        M = np.eye(7) - dt[b] * J[b]
+        lu, _, _ = linalg.lu_factor(M, check_singular=False)
+        ratio[b] = np.min(np.abs(np.diag(lu))) / np.max(np.abs(M))
+        try:
+            linalg.lu_factor(M, check_singular=True)
+        except linalg.SingularMatrixError:
+            singular[b] = True
+    print("tangent singular cases:", int(singular.sum()), "of", B)
+    save("tangent_singular.npz", eps_n=eps_n, eps_np1=eps_np1, a=a, dt=dt, singular=singular, ratio=ratio)
+
+
 def make_radial_stall():
     """A Michel-Suquet parameter set (n = 10, small sigma_d) whose radial
     return stalls (gsm.py:377-378 NewtonError) at eps_n = 0, a_n = 0: the
@@ -664,6 +697,7 @@ if __name__ == "__main__":
         "path8_ode23": make_path8_ode23,
         "path8_ode23_fail": make_path8_ode23_fail,
         "radial": make_radial_stall,
+        "tangent_singular": make_tangent_singular,
         "path32": lambda: make_path_conv(32),
         "path64": lambda: make_path_conv(64),
     }

@@ -82,6 +82,24 @@ extern "C" int hostcheck_eval(int kind, const double* prm, int mode, double tol,
     return run(L, cfg, B, eps_n, a_n, eps_np1, dt, want_tangent, sig, a_out, C, iters, status);
 }
 
+// the tangent post-process alone at a given (unclamped, "converged") state:
+// the singular-tangent route (odeint.py:424 check_singular) without a Newton
+extern "C" int hostcheck_tangent_point(const double* prm, int64_t B, const double* eps_n, const double* a,
+                                       const double* eps_np1, const double* dt, double* sig, double* C,
+                                       uint8_t* status) {
+    auto L = MichelSuquetLaw::make(prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], prm[6]);
+    int any = 0;
+    for (int64_t b = 0; b < B; ++b) {
+        double ac[7], Cv[6][6];
+        HostSink sink{Cv};
+        const int st = tangent_point(L, eps_n + 6 * b, eps_np1 + 6 * b, dt[b], a + 7 * b, ac, sig + 6 * b, sink);
+        std::memcpy(C + 36 * b, Cv, sizeof(Cv));
+        status[b] = (uint8_t)st;
+        any |= st;
+    }
+    return any;
+}
+
 // adaptive ode12 / ode23 (material.cu k_adaptive on the host)
 #include "../../paper_2006_04391_b200/csrc/adaptive.cuh"
 
