@@ -3,9 +3,9 @@ reference: gsmkit (installed unmodified into baseline/_ref by
 __graft_entry__.build()) gets the documented ctypes block exec'd into its
 evaluator module and the documented two-line hook in evaluate_arrays; then
 the reference's OWN Homogenizer / solve_step / evaluate_field / commit_step
-run config 1 and the first steps of the 8^3 path with every material
-evaluation on libautomat.so, against the fixtures the unmodified reference
-produced (tests/golden)."""
+run config 1, the first steps of the 8^3 path and its run_loading_path the
+full 16^3 20-step path with every material evaluation on libautomat.so,
+against the fixtures the unmodified reference produced (tests/golden)."""
 
 import os
 import re
@@ -109,3 +109,21 @@ def test_reference_homogenizer_path8_on_gpu(gsmkit):
     assert rel(hom.eps_n, g["eps_n"]) < 1e-10
     assert rel(grid.state[0], g["state0"]) < 1e-10
     assert calls["cpu"] == cpu0
+
+
+def test_reference_run_loading_path16_on_gpu(gsmkit):
+    """The reference's own run_loading_path (homogenize.py:485-528) at 16^3,
+    20 steps, every material evaluation (iterations and tangent sweeps) on
+    libautomat through the binding: the reference fixture's iteration counts
+    and records (path16_conv.npz)."""
+    ev, gsm, H, calls = gsmkit
+    g = golden("path16_conv.npz")
+    cfg = ev.StrategyConfig(strategy="automatic", integrator="implicit-euler")
+    cpu0, gpu0 = calls["cpu"], calls["gpu"]
+    recs = H.run_loading_path(H.toy_mmc_grid(16), H.LoadingPath(steps=20), cfg)
+    assert calls["cpu"] == cpu0 and calls["gpu"] - gpu0 >= 2 * int(g["iterations"].sum())
+    assert [r["iterations"] for r in recs] == g["iterations"].tolist()
+    sig = np.stack([r["sig"] for r in recs])
+    assert float(np.max(np.abs(sig - g["sig"]).max(axis=1) / np.abs(g["sig"]).max(axis=1))) <= 1e-10
+    assert rel([r["C11"] for r in recs], g["C11"]) <= 1e-8
+    assert rel([r["eps_xx"] for r in recs], g["eps_xx"]) <= 1e-10
