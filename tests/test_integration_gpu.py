@@ -127,3 +127,24 @@ def test_reference_run_loading_path16_on_gpu(gsmkit):
     assert float(np.max(np.abs(sig - g["sig"]).max(axis=1) / np.abs(g["sig"]).max(axis=1))) <= 1e-10
     assert rel([r["C11"] for r in recs], g["C11"]) <= 1e-8
     assert rel([r["eps_xx"] for r in recs], g["eps_xx"]) <= 1e-10
+
+
+def test_reference_evaluate_arrays_every_route_on_gpu(gsmkit):
+    """Through the binding, every strategy x integrator the reference accepts
+    runs on libautomat and matches the reference's own CPU route (the
+    original evaluate_arrays on the same inputs)."""
+    ev, gsm, H, calls = gsmkit
+    from paper_2006_04391_b200.workloads import config2_batch
+
+    en, an, ep, dt = config2_batch(64, seed=4)
+    law = gsm.MichelSuquet()
+    for strat, integ in (("automatic", "implicit-euler"), ("semi-automatic", "implicit-euler"),
+                         ("conventional", "implicit-euler"), ("automatic", "ode23"), ("semi-automatic", "ode23s")):
+        cfg = ev.StrategyConfig(strategy=strat, integrator=integ)
+        g0 = calls["gpu"]
+        r = ev.evaluate_arrays(law, cfg, en, an, ep, dt, want_tangent=True)
+        assert calls["gpu"] == g0 + 1, (strat, integ)
+        ref = ev._evaluate_chunk(law, cfg, en, an, ep, np.broadcast_to(dt, (len(dt),)).copy(), True)
+        assert rel(r.sigma, ref.sigma) <= 1e-10 and rel(r.a, ref.a) <= 1e-10, (strat, integ)
+        assert rel(r.C, ref.C) <= 1e-8, (strat, integ)
+        assert np.array_equal(r.substeps, ref.substeps) and np.array_equal(r.rejected, ref.rejected), (strat, integ)
