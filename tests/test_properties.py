@@ -1,0 +1,140 @@
+"""Homogenizer known answers and size-independent properties (SPEC.md
+acceptance criterion 9), on the numpy oracle (CPU) and on the device basic
+scheme (GPU):
+
+* a two-phase elastic laminate reproduces the closed-form effective
+  stiffness (tests/_laminate.py) for layers normal to x, y and z, also with
+  the x-slab algorithm cutting across the layers;
+* a homogeneous grid converges in one iteration with sigma = C eps_bar;
+* Hill-Mandel: <sigma . eps> = sigma_bar . eps_bar on converged elastic solves;
+* the effective stiffness of the (anisotropic) fibre composite has major
+  symmetry;
+* linearity: doubling eps_bar on an elastic grid doubles every field
+  bitwise with the same iteration count (powers of two scale exactly
+  through the material law, the FFTs and the Green operator).
+The grid is elastic throughout, so these hold to solver tolerance (1e-10 here).
+"""
+
+import numpy as np
+import pytest
+
+from _laminate import laminate_ids, laminate_stiffness
+
+PHASES = [(55e9, 0.33), (300e9, 0.25)]  # config 1's matrix / fibre
+TOL = 1e-10
+
+
+def rel(x, y):
+    x, y = np.asarray(x, float), np.asarray(y, float)
+    return float(np.max(np.abs(x - y)) / max(np.max(np.abs(y)), 1e-300))
+
+
+def hill_mandel(eps, sig):
+    work = float((sig * eps).sum(axis=0).mean())
+    return abs(work - float(sig.mean(axis=(1, 2, 3)) @ eps.mean(axis=(1, 2, 3)))) / abs(work)
+
+
+def toy_ids(n):
+    from paper_2006_04391_b200 import homogenize as H
+
+    return H.toy_mmc_grid(n).material_ids
+
+
+# -- oracle (CPU): pins the closed forms and the properties on the restatement
+
+
+def _oracle_basic(ids):
+    from oracle import homogenize as OH
+    from oracle import material as OM
+
+    return OH.Basic(ids, [OM.law_params(0, *p) for p in PHASES], tol=TOL, threads=1)
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_oracle_laminate(axis):
+    b = _oracle_basic(laminate_ids(8, axis, 2))
+    C = np.stack([b.solve_step(np.eye(6)[j] * 1e-3, 1.0)[1].mean(axis=(1, 2, 3)) / 1e-3 for j in range(6)], axis=1)
+    assert rel(C, laminate_stiffness(PHASES, [0.75, 0.25], axis)) < 1e-9
+
+
+def test_oracle_hill_mandel_and_symmetry():
+    b = _oracle_basic(toy_ids(8))
+    cols = []
+    for j in range(6):
+        eps, sig, it, _ = b.solve_step(np.eye(6)[j] * 1e-3, 1.0)
+        assert hill_mandel(eps, sig) < 1e-8
+        cols.append(sig.mean(axis=(1, 2, 3)) / 1e-3)
+    C = np.stack(cols, axis=1)
+    assert rel(C, C.T) < 1e-8
+
+
+# -- device basic scheme
+
+
+def _homogenizer(ids, slabs=1, max_iterations=5000):
+    from paper_2006_04391_b200 import gsm
+    from paper_2006_04391_b200 import homogenize as H
+    from paper_2006_04391_b200.evaluator import StrategyConfig
+
+    laws = [gsm.LinearElastic(*p) for p in PHASES][: int(ids.max()) + 1]
+    grid = H.VoxelGrid(ids, laws)
+    return H.Homogenizer(grid, StrategyConfig(strategy="automatic", integrator="implicit-euler"), tol=TOL,
+                         max_iterations=max_iterations, slabs=slabs)
+
+
+def _stiffness(hom):
+    cols = []
+    for j in range(6):
+        eps, sig, info = hom.solve_step(np.eye(6)[j] * 1e-3, 1.0)
+        cols.append(sig.mean(axis=(1, 2, 3)) / 1e-3)
+    return np.stack(cols, axis=1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("slabs", [1, 2])
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_laminate_gpu(axis, slabs):
+    C = _stiffness(_homogenizer(laminate_ids(16, axis, 4), slabs=slabs))
+    assert rel(C, laminate_stiffness(PHASES, [0.75, 0.25], axis)) < 1e-9
+
+
+@pytest.mark.gpu
+def test_homogeneous_grid_one_iteration_gpu():
+    from _laminate import lame
+
+    hom = _homogenizer(np.zeros((16, 16, 16), np.uint8))
+    rng = np.random.default_rng(9)
+    eb = rng.uniform(-1e-3, 1e-3, 6)
+    eps, sig, info = hom.solve_step(eb, 1.0)
+    assert info.iterations == 1
+    lam, mu = lame(*PHASES[0])
+    C = np.zeros((6, 6))
+    C[:3, :3] = lam
+    C[np.arange(3), np.arange(3)] += 2.0 * mu
+    C[np.arange(3, 6), np.arange(3, 6)] = mu
+    assert rel(sig.reshape(6, -1), (C @ eb)[:, None] * np.ones((1, 16 ** 3))) < 1e-14
+    assert rel(eps.reshape(6, -1), eb[:, None] * np.ones((1, 16 ** 3))) == 0.0
+
+
+@pytest.mark.gpu
+def test_hill_mandel_and_symmetry_gpu():
+    hom = _homogenizer(toy_ids(16))
+    cols = []
+    for j in range(6):
+        eps, sig, info = hom.solve_step(np.eye(6)[j] * 1e-3, 1.0)
+        assert hill_mandel(eps, sig) < 1e-8
+        cols.append(sig.mean(axis=(1, 2, 3)) / 1e-3)
+    C = np.stack(cols, axis=1)
+    assert rel(C, C.T) < 1e-8
+    assert np.all(np.linalg.eigvalsh(0.5 * (C + C.T)) > 0)
+
+
+@pytest.mark.gpu
+def test_linearity_bitwise_gpu():
+    ids = toy_ids(16)
+    eb = np.array([1e-3, -3e-4, 2e-4, 5e-4, -1e-4, 3e-4])
+    eps1, sig1, info1 = _homogenizer(ids).solve_step(eb, 1.0)
+    eps2, sig2, info2 = _homogenizer(ids).solve_step(2.0 * eb, 1.0)
+    assert info1.iterations == info2.iterations
+    np.testing.assert_array_equal(eps2, 2.0 * eps1)
+    np.testing.assert_array_equal(sig2, 2.0 * sig1)
