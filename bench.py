@@ -261,7 +261,11 @@ def basic_step(grid, n, dev, dist=None, comm=None, warm=False, max_iterations=50
     Nh = n * n * (n // 2 + 1) // world  # rfft bins per rank
     it_t = ph[4] or 1.0
     fourier_ms = ph[2] / it_t
-    fourier_bytes = 4 * 96.0 * Nh  # read shat, ehat; write ehat, shat (complex128 x 6)
+    zcb = ctypes.c_int(0)
+    _lib.check(lib.am_solver_fft_callback(hom._h, ctypes.byref(zcb)))
+    # read shat, ehat; write ehat (complex128 x 6), and without the inverse
+    # transform's load callback also the scaled copy ehat'/N into shat
+    fourier_bytes = (3 if zcb.value else 4) * 96.0 * Nh
     out = {
         "value": iters / (ms * 1e-3), "unit": "it/s", "iterations": iters, "ms_total": ms,
         "ms_per_iteration": ms / iters,
@@ -271,6 +275,7 @@ def basic_step(grid, n, dev, dist=None, comm=None, warm=False, max_iterations=50
                              "peak": hbm_peak(), "unit": "GB/s",
                              "frac": fourier_bytes / (fourier_ms * 1e-3) / 1e9 / hbm_peak(),
                              "traffic_per_launch_algorithmic": fourier_bytes},
+        "fft_load_callback": bool(zcb.value),
         "clocks": clk.summary(),
     }
     if capped:

@@ -244,6 +244,12 @@ int am_solver_solve_step(am_solver *h, const double *ebar_target, double dt, con
  * agree with the cold start to round-off, not bit for bit.  No reference
  * counterpart (the reference always starts at a_n, odeint.py:371). */
 int am_solver_set_warm_start(am_solver *h, int on);
+/* 1 in *on if the solver's inverse transform reads the carried spectrum
+ * through a cuFFT load callback (one slab, power-of-two voxel counts from
+ * 128^3 on, or AM_FFT_CALLBACK=1; fields bitwise those of the copy path),
+ * else 0.  No
+ * reference counterpart (implementation detail of homogenize.py:458-460). */
+int am_solver_fft_callback(const am_solver *h, int *on);
 /* Homogenizer.commit_step (homogenize.py:474-480) for the solver's eps:
  * eps_n <- eps, ebar_n <- ebar and, if a solve_step converged since the
  * last commit, the internal state <- that step's state (evaluations in

@@ -131,6 +131,7 @@ SIGNATURES = {
     ]),
     "am_solver_commit": (ctypes.c_int, [_vp, _dp]),
     "am_solver_set_warm_start": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "am_solver_fft_callback": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
     "am_solver_evaluate": (ctypes.c_int, [_vp, ctypes.c_double]),
     "am_solver_tangent_sweep": (ctypes.c_int, [_vp, ctypes.c_double, _dp, _dp, _dp]),
     "am_solver_get_field": (ctypes.c_int, [_vp, ctypes.c_int, _dp]),

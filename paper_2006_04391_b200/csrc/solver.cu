@@ -39,6 +39,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fft_cb.h"
 #include "fourier.cuh"
 #include "k1.cuh"
 #include "laws.cuh"
@@ -113,7 +114,9 @@ __global__ void k_shift(double* __restrict__ eps, const double* __restrict__ eps
 // K2: residual partials + Green update for every bin of the slab but the
 // global origin.  Block b handles part (b % kParts) of ky plane (b / kParts);
 // its partial goes to red[(y0 + kyl) * kParts + part].
-// S: rfft(sigma) in, ehat'/N out;  ehat: rfft(eps) in, ehat' out.
+// S: rfft(sigma) in, ehat'/N out (scaled = 0: S untouched, the inverse
+// transform reads ehat' / N through its load callback, fft_cb.cu);
+// ehat: rfft(eps) in, ehat' out.
 #ifndef AM_FOURIER_MINB
 #define AM_FOURIER_MINB 1
 #endif
@@ -122,7 +125,7 @@ __global__ void k_shift(double* __restrict__ eps, const double* __restrict__ eps
 #endif
 __global__ void __launch_bounds__(kRedThreads, AM_FOURIER_MINB) k_fourier(Spec sp, RefMat ref, double2* __restrict__ S,
                                                          double2* __restrict__ ehat, double* __restrict__ red,
-                                                         int update) {
+                                                         int update, int scaled) {
     __shared__ double sh[kRedThreads / 32];
     const int kyl = blockIdx.x / kParts, part = blockIdx.x % kParts;
     const int ky = sp.y0 + kyl;
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(kRedThreads, AM_FOURIER_MINB) k_fourier(Spec s
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
                 ehat[c * sp.cs + q] = make_double2(outr[c], outi[c]);
-                S[c * sp.cs + q] = make_double2(outr[c] * invN, outi[c] * invN);
+                if (scaled) S[c * sp.cs + q] = make_double2(outr[c] * invN, outi[c] * invN);
             }
         }
     }
@@ -188,7 +191,7 @@ __global__ void __launch_bounds__(kRedThreads, AM_FOURIER_MINB) k_fourier(Spec s
 // results are stored (software pipelining; AM_FOURIER_PF=1)
 __global__ void __launch_bounds__(kRedThreads, AM_FOURIER_MINB) k_fourier_pf(Spec sp, RefMat ref, double2* __restrict__ S,
                                                             double2* __restrict__ ehat, double* __restrict__ red,
-                                                            int update) {
+                                                            int update, int scaled) {
     __shared__ double sh[kRedThreads / 32];
     const int kyl = blockIdx.x / kParts, part = blockIdx.x % kParts;
     const int ky = sp.y0 + kyl;
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(kRedThreads, AM_FOURIER_MINB) k_fourier_pf(Spe
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
                 ehat[c * sp.cs + q] = make_double2(outr[c], outi[c]);
-                S[c * sp.cs + q] = make_double2(outr[c] * invN, outi[c] * invN);
+                if (scaled) S[c * sp.cs + q] = make_double2(outr[c] * invN, outi[c] * invN);
             }
         }
     }
@@ -293,12 +296,13 @@ __global__ void k_origin(double2* S, double2* ehat, int64_t cs, Vec6 ebar, doubl
     }
 }
 
-// the same with the mean strain read from device memory (graph replays)
+// the same with the mean strain read from device memory (graph replays;
+// S = nullptr: the inverse transform's load callback reads ebar itself)
 __global__ void k_origin_dev(double2* S, double2* ehat, int64_t cs, const double* __restrict__ ebar, double N) {
     const int c = threadIdx.x;
     if (c < 6) {
         ehat[c * cs] = make_double2(ebar[c] * N, 0.0);
-        S[c * cs] = make_double2(ebar[c], 0.0);
+        if (S) S[c * cs] = make_double2(ebar[c], 0.0);
     }
 }
 
@@ -624,6 +628,8 @@ struct am_solver {
     ncclComm_t comm = nullptr;  // nccl mode: this process holds one slab
     std::vector<am::Slab> slabs;  // slabs held by this process
     cufftHandle r3 = 0, c3 = 0;   // 3-D D2Z / Z2D (single slab)
+    bool zcb = false;             // c3 reads ehat' / N and the origin through a load callback (fft_cb.cu)
+    void* d_cbinfo = nullptr;     // its AmZ2DCb
     cufftHandle r2 = 0, c2 = 0;   // 2-D D2Z / Z2D over (y, z), batch 6 nxl
     cufftHandle x1 = 0;           // 1-D Z2Z over x, batch 6 nyl nzh
     double* red = nullptr;        // reduction vectors, one per local slab, length redlen
@@ -677,7 +683,7 @@ static void solver_free(am_solver* h) {
     cudaFree(h->red); cudaFreeHost(h->hred);
     cudaFree(h->Cbuf); cudaFree(h->status); cudaFree(h->stats); cudaFreeHost(h->hstats); cudaFree(h->dsmall);
     cudaFree(h->pl); cudaFreeHost(h->hpl); cudaFree(h->ps); cudaFreeHost(h->hps);
-    cudaFree(h->d_eb); cudaFreeHost(h->h_eb);
+    cudaFree(h->d_eb); cudaFreeHost(h->h_eb); cudaFree(h->d_cbinfo);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     for (cufftHandle p : {h->r3, h->c3, h->r2, h->c2, h->x1})
@@ -837,9 +843,11 @@ static int fourier_enqueue(am_solver* h, bool update) {
 #define AM_FOURIER_PF 0
 #endif
         if (AM_FOURIER_PF)
-            k_fourier_pf<<<s.sp.nyl * kParts, kRedThreads, 0, h->stream>>>(s.sp, ref, s.S, s.ehat, red, update ? 1 : 0);
+            k_fourier_pf<<<s.sp.nyl * kParts, kRedThreads, 0, h->stream>>>(s.sp, ref, s.S, s.ehat, red, update ? 1 : 0,
+                                                                            h->zcb ? 0 : 1);
         else
-            k_fourier<<<s.sp.nyl * kParts, kRedThreads, 0, h->stream>>>(s.sp, ref, s.S, s.ehat, red, update ? 1 : 0);
+            k_fourier<<<s.sp.nyl * kParts, kRedThreads, 0, h->stream>>>(s.sp, ref, s.S, s.ehat, red, update ? 1 : 0,
+                                                                         h->zcb ? 0 : 1);
         AM_CUDA(cudaGetLastError());
         k_finish<<<1, 32, 0, h->stream>>>(s.S, s.sp.cs, s.y0 == 0 ? 1 : 0, s.flags, s.subs, red,
                                           (int64_t)h->ny * kParts);
@@ -1038,8 +1046,23 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
     bool ok;
     if (!h->multi) {
         long long n3[3] = {nx, ny, nz};
-        ok = plan(&h->r3, 3, n3, nullptr, 1, N, nullptr, 1, (long long)nx * ny * h->nzh, CUFFT_D2Z, 6) &&
-             plan(&h->c3, 3, n3, nullptr, 1, (long long)nx * ny * h->nzh, nullptr, 1, N, CUFFT_Z2D, 6);
+        ok = plan(&h->r3, 3, n3, nullptr, 1, N, nullptr, 1, (long long)nx * ny * h->nzh, CUFFT_D2Z, 6);
+        // the inverse transform with the load callback (fft_cb.cu) from 128^3
+        // on, where the saved copy matters, for power-of-two voxel counts
+        // (the origin's N ebar / N is then exact); AM_FFT_CALLBACK=0 / 1
+        // forces it off / on.  The callback's first link in a process costs ~2 s.
+        const char* cb = getenv("AM_FFT_CALLBACK");
+        const bool pow2 = (N & (N - 1)) == 0;
+        const bool want = !h->xfused && pow2 && (cb ? cb[0] == '1' : N >= (int64_t(1) << 21));
+        if (ok && want) {
+            const am::Slab& s0 = h->slabs[0];
+            const AmZ2DCb info{s0.ehat, 1.0 / (double)N};
+            h->zcb = cudaMalloc(&h->d_cbinfo, sizeof(info)) == cudaSuccess &&
+                     cudaMemcpy(h->d_cbinfo, &info, sizeof(info), cudaMemcpyHostToDevice) == cudaSuccess &&
+                     am_z2d_callback_plan(&h->c3, n3, (long long)nx * ny * h->nzh, N, 6, h->stream, h->d_cbinfo);
+        }
+        if (ok && !h->zcb)
+            ok = plan(&h->c3, 3, n3, nullptr, 1, (long long)nx * ny * h->nzh, nullptr, 1, N, CUFFT_Z2D, 6);
         if (ok && h->xfused) {
             long long n2[2] = {ny, nz};
             ok = plan(&h->r2, 2, n2, nullptr, 1, (long long)ny * nz, nullptr, 1, (long long)ny * h->nzh, CUFFT_D2Z,
@@ -1251,7 +1274,7 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
         Slab& s0 = h->slabs[0];
         AM_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
         auto body = [&]() -> int {
-            k_origin_dev<<<1, 32, 0, h->stream>>>(s0.S, s0.ehat, s0.sp.cs, h->d_eb, Nd);
+            k_origin_dev<<<1, 32, 0, h->stream>>>(h->zcb ? nullptr : s0.S, s0.ehat, s0.sp.cs, h->d_eb, Nd);
             AM_CUDA(cudaGetLastError());
             AM_TRY(inverse(h, &Slab::S, &Slab::eps));
             AM_TRY(material_sweep(h, dt, h->warm_start));
@@ -1362,6 +1385,13 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
             k_origin_x<<<6, 256, 0, h->stream>>>(s.S, s.ehat, s.sp.cs, (int64_t)h->ny * h->nzh, h->nx, eb, Nd);
             AM_CUDA(cudaGetLastError());
             AM_CUFFT(cufftExecZ2D(h->c2, s.S, s.eps));
+        } else if (h->zcb) {  // the callback reads the origin's N ebar from ehat
+            Slab& s0 = h->slabs[0];
+            for (int i = 0; i < 6; ++i) h->h_eb[i] = ebar[i];
+            AM_CUDA(cudaMemcpyAsync(h->d_eb, h->h_eb, sizeof(double) * 6, cudaMemcpyHostToDevice, h->stream));
+            k_origin_dev<<<1, 32, 0, h->stream>>>(nullptr, s0.ehat, s0.sp.cs, h->d_eb, Nd);
+            AM_CUDA(cudaGetLastError());
+            AM_TRY(inverse(h, &Slab::S, &Slab::eps));
         } else {
             for (auto& s : h->slabs)
                 if (s.y0 == 0) {
@@ -1383,6 +1413,12 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
 extern "C" int am_solver_set_warm_start(am_solver* h, int on) {
     if (!h) return fail(AM_ERR_ARG, "null solver");
     h->warm_start = on != 0;
+    return AM_OK;
+}
+
+extern "C" int am_solver_fft_callback(const am_solver* h, int* on) {
+    if (!h || !on) return fail(AM_ERR_ARG, "null argument");
+    *on = h->zcb ? 1 : 0;
     return AM_OK;
 }
 
@@ -1706,7 +1742,7 @@ extern "C" int am_equilibrium_residual_host(int nx, int ny, int nz, const double
         rc = fail(AM_ERR_CUDA, "copy failed");
     if (rc == AM_OK && cufftExecD2Z(p1, f, c) != CUFFT_SUCCESS) rc = fail(AM_ERR_CUDA, "D2Z failed");
     if (rc == AM_OK) {
-        k_fourier<<<ny * kParts, kRedThreads>>>(sp, RefMat::make(1.0, 1.0), c, nullptr, red, 0);
+        k_fourier<<<ny * kParts, kRedThreads>>>(sp, RefMat::make(1.0, 1.0), c, nullptr, red, 0, 0);
         k_finish<<<1, 32>>>(c, sp.cs, 1, nullptr, nullptr, red, (int64_t)ny * kParts);
         if (cudaMemcpy(o.data(), red, sizeof(double) * L, cudaMemcpyDeviceToHost) != cudaSuccess)
             rc = fail(AM_ERR_CUDA, "residual kernel failed");

@@ -417,3 +417,63 @@ def test_graph_replay_bitwise_equal_to_eager(H, AUTO):
         out.append(res)
     for (e0, s0, h0), (e1, s1, h1) in zip(*out):
         assert np.array_equal(e0, e1) and np.array_equal(s0, s1) and h0 == h1
+
+
+@pytest.mark.parametrize("graphs", ["0", "1"])
+def test_fft_callback_bitwise_equal_to_copy(H, AUTO, graphs):
+    """The inverse transform reading ehat'/N and the origin through a cuFFT
+    load callback (fft_cb.cu; AM_FFT_CALLBACK=1 forces it below 128^3)
+    gives bitwise the fields and histories of the path where k_fourier
+    writes the scaled copy, eager and as graph replays, mixed BC."""
+    import ctypes
+    import os
+
+    from paper_2006_04391_b200 import _lib
+
+    out = []
+    for cb in ("0", "1"):
+        os.environ["AM_FFT_CALLBACK"] = cb
+        os.environ["AM_NO_GRAPHS"] = "0" if graphs == "1" else "1"
+        try:
+            hom = H.Homogenizer(H.toy_mmc_grid(16), AUTO)
+        finally:
+            os.environ.pop("AM_FFT_CALLBACK", None)
+            os.environ.pop("AM_NO_GRAPHS", None)
+        on = ctypes.c_int(-1)
+        _lib.check(hom._lib.am_solver_fft_callback(hom._h, ctypes.byref(on)))
+        assert on.value == int(cb), "the cuFFT load callback did not link in this process"
+        path = H.LoadingPath(steps=20)
+        t = path.times()
+        res = []
+        for k in (1, 2, 3):
+            eb = np.zeros(6)
+            eb[0] = path.eps_xx(t[k])
+            eps, sig, info = hom.solve_step(eb, t[k] - t[k - 1], free_mask=np.array([False] + [True] * 5))
+            res.append((eps, sig, info.history))
+            hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+        out.append(res)
+    for (e0, s0, h0), (e1, s1, h1) in zip(*out):
+        assert np.array_equal(e0, e1) and np.array_equal(s0, s1) and h0 == h1
+
+
+def test_fft_callback_default_from_128(H, AUTO):
+    """Power-of-two grids from 128^3 on take the callback path by default;
+    other voxel counts never do (the origin's N ebar / N must be exact)."""
+    import ctypes
+
+    hom = H.Homogenizer(H.toy_mmc_grid(128), AUTO)
+    on = ctypes.c_int(-1)
+    hom._lib.am_solver_fft_callback(hom._h, ctypes.byref(on))
+    assert on.value == 1
+    small = H.Homogenizer(H.toy_mmc_grid(16), AUTO)
+    small._lib.am_solver_fft_callback(small._h, ctypes.byref(on))
+    assert on.value == 0
+    import os
+
+    os.environ["AM_FFT_CALLBACK"] = "1"
+    try:
+        odd = H.Homogenizer(H.toy_mmc_grid(12), AUTO)
+    finally:
+        os.environ.pop("AM_FFT_CALLBACK", None)
+    odd._lib.am_solver_fft_callback(odd._h, ctypes.byref(on))
+    assert on.value == 0
