@@ -245,9 +245,9 @@ int am_solver_solve_step(am_solver *h, const double *ebar_target, double dt, con
  * counterpart (the reference always starts at a_n, odeint.py:371). */
 int am_solver_set_warm_start(am_solver *h, int on);
 /* 1 in *on if the solver's inverse transform reads the carried spectrum
- * through a cuFFT load callback (one slab, power-of-two voxel counts from
- * 128^3 on, or AM_FFT_CALLBACK=1; fields bitwise those of the copy path),
- * else 0.  No
+ * through a cuFFT load callback (the 3-D inverse on one slab, every slab's
+ * inverse x transform on x slabs; power-of-two voxel counts from 128^3 on,
+ * or AM_FFT_CALLBACK=1; fields bitwise those of the copy path), else 0.  No
  * reference counterpart (implementation detail of homogenize.py:458-460). */
 int am_solver_fft_callback(const am_solver *h, int *on);
 /* Homogenizer.commit_step (homogenize.py:474-480) for the solver's eps:

@@ -1,5 +1,6 @@
 // fft_cb.cu -- the basic scheme's inverse transform reading the carried
-// spectrum through a cuFFT load callback (single slab, 3-D Z2D).
+// spectrum through a cuFFT load callback (one slab: the 3-D Z2D; x slabs:
+// each slab's inverse 1-D x transform).
 //
 // k_fourier leaves ehat' (the carried spectrum of the next strain) in ehat;
 // the Z2D destroys its input, so without a callback k_fourier also writes a
@@ -109,11 +110,13 @@ size_t g_next = 0;
 
 }  // namespace
 
-// cufft plan *p (created here) for the batch-6 3-D Z2D with the load
-// callback reading through d_info (a device AmZ2DCb).  Returns false, with
-// *p = 0, if the callback cannot be linked in this process.
-bool am_z2d_callback_plan(cufftHandle* p, long long* n3, long long idist, long long odist, long long batch,
-                          cudaStream_t stream, void* d_info) {
+// cufft plan *p (created here; cufftMakePlanMany64 geometry) whose first
+// pass loads its complex input through the callback reading d_info (a
+// device AmZ2DCb).  Returns false, with *p = 0, if the callback cannot be
+// linked in this process.
+bool am_callback_plan(cufftHandle* p, int rank, long long* n, long long* inembed, long long istride, long long idist,
+                      long long* onembed, long long ostride, long long odist, cufftType type, long long batch,
+                      cudaStream_t stream, void* d_info) {
     std::lock_guard<std::mutex> lk(g_mu);
     *p = 0;
     if (g_state == 0) g_cands = nvrtc_candidates();
@@ -132,8 +135,8 @@ bool am_z2d_callback_plan(cufftHandle* p, long long* n3, long long idist, long l
         bool ok = cufftCreate(&h) == CUFFT_SUCCESS &&
                   cufftXtSetJITCallback(h, "am_z2d_load", g_ir.data(), g_ir.size(), CUFFT_CB_LD_COMPLEX_DOUBLE,
                                         &info) == CUFFT_SUCCESS &&
-                  cufftMakePlanMany64(h, 3, n3, nullptr, 1, idist, nullptr, 1, odist, CUFFT_Z2D, batch, &ws) ==
-                      CUFFT_SUCCESS &&
+                  cufftMakePlanMany64(h, rank, n, inembed, istride, idist, onembed, ostride, odist, type, batch,
+                                      &ws) == CUFFT_SUCCESS &&
                   cufftSetStream(h, stream) == CUFFT_SUCCESS;
         if (ok) {
             *p = h;

@@ -9,5 +9,6 @@ struct AmZ2DCb {
     double inv_n;         // 1 / (nx ny nz), a power of two
 };
 
-bool am_z2d_callback_plan(cufftHandle* p, long long* n3, long long idist, long long odist, long long batch,
-                          cudaStream_t stream, void* d_info);
+bool am_callback_plan(cufftHandle* p, int rank, long long* n, long long* inembed, long long istride, long long idist,
+                      long long* onembed, long long ostride, long long odist, cufftType type, long long batch,
+                      cudaStream_t stream, void* d_info);

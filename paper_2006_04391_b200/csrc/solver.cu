@@ -609,6 +609,8 @@ struct Slab {
     unsigned long long* subs = nullptr;  // accepted substeps of the last sweep (adaptive integrators)
     double2** peerS = nullptr;  // device arrays: every rank's S / ehat (P2P transport)
     double2** peerE = nullptr;
+    cufftHandle x1i = 0;        // inverse x transform reading ehat' / N through the load callback
+    void* d_cbinfo = nullptr;   // its AmZ2DCb
     std::vector<Phase> phases;
 };
 
@@ -628,8 +630,9 @@ struct am_solver {
     ncclComm_t comm = nullptr;  // nccl mode: this process holds one slab
     std::vector<am::Slab> slabs;  // slabs held by this process
     cufftHandle r3 = 0, c3 = 0;   // 3-D D2Z / Z2D (single slab)
-    bool zcb = false;             // c3 reads ehat' / N and the origin through a load callback (fft_cb.cu)
-    void* d_cbinfo = nullptr;     // its AmZ2DCb
+    bool zcb = false;             // the inverse transform reads ehat' / N through a load callback (fft_cb.cu):
+                                  // c3 (one slab) or every slab's x1i
+    void* d_cbinfo = nullptr;     // c3's AmZ2DCb
     cufftHandle r2 = 0, c2 = 0;   // 2-D D2Z / Z2D over (y, z), batch 6 nxl
     cufftHandle x1 = 0;           // 1-D Z2Z over x, batch 6 nyl nzh
     double* red = nullptr;        // reduction vectors, one per local slab, length redlen
@@ -678,7 +681,8 @@ static void solver_free(am_solver* h) {
         }
         cudaFree(s.eps); cudaFree(s.eps_n); cudaFree(s.sigma);
         cudaFree(s.S); cudaFree(s.ehat); cudaFree(s.P); cudaFree(s.X); cudaFree(s.flags); cudaFree(s.subs);
-        cudaFree(s.peerS); cudaFree(s.peerE);
+        cudaFree(s.peerS); cudaFree(s.peerE); cudaFree(s.d_cbinfo);
+        if (s.x1i) cufftDestroy(s.x1i);
     }
     cudaFree(h->red); cudaFreeHost(h->hred);
     cudaFree(h->Cbuf); cudaFree(h->status); cudaFree(h->stats); cudaFreeHost(h->hstats); cudaFree(h->dsmall);
@@ -784,7 +788,9 @@ static int inverse(am_solver* h, double2* Slab::*src, double* Slab::*field) {
         AM_CUFFT(cufftExecZ2D(h->c3, s.*src, s.*field));
         return AM_OK;
     }
-    for (auto& s : h->slabs) AM_CUFFT(cufftExecZ2Z(h->x1, s.*src, s.*src, CUFFT_INVERSE));
+    // S: the load callback reads ehat' / N instead (the caller skipped the copy)
+    for (auto& s : h->slabs)
+        AM_CUFFT(cufftExecZ2Z(h->zcb && src == &Slab::S ? s.x1i : h->x1, s.*src, s.*src, CUFFT_INVERSE));
     if (h->p2p) {
         AM_TRY(barrier(h));  // every rank's x-transform is done before it is read
         for (auto& s : h->slabs) {
@@ -1044,22 +1050,22 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
                cufftSetStream(*p, h->stream) == CUFFT_SUCCESS;
     };
     bool ok;
+    // the inverse transform with the load callback (fft_cb.cu) from 128^3
+    // on, where the saved copy matters, for power-of-two voxel counts (the
+    // origin's N ebar / N is then exact); AM_FFT_CALLBACK=0 / 1 forces it
+    // off / on.  The callback's first link in a process costs ~2 s.
+    const char* cbenv = getenv("AM_FFT_CALLBACK");
+    const bool want_cb = !h->xfused && (N & (N - 1)) == 0 && (cbenv ? cbenv[0] == '1' : N >= (int64_t(1) << 21));
     if (!h->multi) {
         long long n3[3] = {nx, ny, nz};
         ok = plan(&h->r3, 3, n3, nullptr, 1, N, nullptr, 1, (long long)nx * ny * h->nzh, CUFFT_D2Z, 6);
-        // the inverse transform with the load callback (fft_cb.cu) from 128^3
-        // on, where the saved copy matters, for power-of-two voxel counts
-        // (the origin's N ebar / N is then exact); AM_FFT_CALLBACK=0 / 1
-        // forces it off / on.  The callback's first link in a process costs ~2 s.
-        const char* cb = getenv("AM_FFT_CALLBACK");
-        const bool pow2 = (N & (N - 1)) == 0;
-        const bool want = !h->xfused && pow2 && (cb ? cb[0] == '1' : N >= (int64_t(1) << 21));
-        if (ok && want) {
+        if (ok && want_cb) {
             const am::Slab& s0 = h->slabs[0];
             const AmZ2DCb info{s0.ehat, 1.0 / (double)N};
             h->zcb = cudaMalloc(&h->d_cbinfo, sizeof(info)) == cudaSuccess &&
                      cudaMemcpy(h->d_cbinfo, &info, sizeof(info), cudaMemcpyHostToDevice) == cudaSuccess &&
-                     am_z2d_callback_plan(&h->c3, n3, (long long)nx * ny * h->nzh, N, 6, h->stream, h->d_cbinfo);
+                     am_callback_plan(&h->c3, 3, n3, nullptr, 1, (long long)nx * ny * h->nzh, nullptr, 1, N, CUFFT_Z2D,
+                                      6, h->stream, h->d_cbinfo);
         }
         if (ok && !h->zcb)
             ok = plan(&h->c3, 3, n3, nullptr, 1, (long long)nx * ny * h->nzh, nullptr, 1, N, CUFFT_Z2D, 6);
@@ -1081,6 +1087,16 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
              plan(&h->c2, 2, n2, nullptr, 1, (long long)ny * h->nzh, nullptr, 1, (long long)ny * nz, CUFFT_Z2D,
                   6LL * nxl) &&
              plan(&h->x1, 1, n1, n1, bx, 1, n1, bx, 1, CUFFT_Z2Z, bx);
+        if (ok && want_cb) {  // every local slab's inverse x transform reads its own ehat'
+            bool all = true;
+            for (auto& sl : h->slabs) {
+                const AmZ2DCb info{sl.ehat, 1.0 / (double)N};
+                all = all && cudaMalloc(&sl.d_cbinfo, sizeof(info)) == cudaSuccess &&
+                      cudaMemcpy(sl.d_cbinfo, &info, sizeof(info), cudaMemcpyHostToDevice) == cudaSuccess &&
+                      am_callback_plan(&sl.x1i, 1, n1, n1, bx, 1, n1, bx, 1, CUFFT_Z2Z, bx, h->stream, sl.d_cbinfo);
+            }
+            h->zcb = all;
+        }
     }
     if (!ok) return bail(fail(AM_ERR_CUDA, "cufft plan creation failed for %dx%dx%d / %d slabs", nx, ny, nz, nslabs));
     if (h->multi) {
@@ -1385,7 +1401,7 @@ extern "C" int am_solver_solve_step(am_solver* h, const double* ebar_target, dou
             k_origin_x<<<6, 256, 0, h->stream>>>(s.S, s.ehat, s.sp.cs, (int64_t)h->ny * h->nzh, h->nx, eb, Nd);
             AM_CUDA(cudaGetLastError());
             AM_CUFFT(cufftExecZ2D(h->c2, s.S, s.eps));
-        } else if (h->zcb) {  // the callback reads the origin's N ebar from ehat
+        } else if (h->zcb && !h->multi) {  // the callback reads the origin's N ebar from ehat
             Slab& s0 = h->slabs[0];
             for (int i = 0; i < 6; ++i) h->h_eb[i] = ebar[i];
             AM_CUDA(cudaMemcpyAsync(h->d_eb, h->h_eb, sizeof(double) * 6, cudaMemcpyHostToDevice, h->stream));

@@ -419,12 +419,13 @@ def test_graph_replay_bitwise_equal_to_eager(H, AUTO):
         assert np.array_equal(e0, e1) and np.array_equal(s0, s1) and h0 == h1
 
 
-@pytest.mark.parametrize("graphs", ["0", "1"])
-def test_fft_callback_bitwise_equal_to_copy(H, AUTO, graphs):
-    """The inverse transform reading ehat'/N and the origin through a cuFFT
-    load callback (fft_cb.cu; AM_FFT_CALLBACK=1 forces it below 128^3)
-    gives bitwise the fields and histories of the path where k_fourier
-    writes the scaled copy, eager and as graph replays, mixed BC."""
+@pytest.mark.parametrize("graphs,slabs", [("0", 1), ("1", 1), ("0", 4)])
+def test_fft_callback_bitwise_equal_to_copy(H, AUTO, graphs, slabs):
+    """The inverse transform reading ehat'/N through a cuFFT load callback
+    (fft_cb.cu; AM_FFT_CALLBACK=1 forces it below 128^3) gives bitwise the
+    fields and histories of the path where k_fourier writes the scaled copy:
+    one slab eager and as graph replays, and the x-slab algorithm (each
+    slab's inverse x transform), mixed BC."""
     import ctypes
     import os
 
@@ -435,7 +436,7 @@ def test_fft_callback_bitwise_equal_to_copy(H, AUTO, graphs):
         os.environ["AM_FFT_CALLBACK"] = cb
         os.environ["AM_NO_GRAPHS"] = "0" if graphs == "1" else "1"
         try:
-            hom = H.Homogenizer(H.toy_mmc_grid(16), AUTO)
+            hom = H.Homogenizer(H.toy_mmc_grid(16), AUTO, slabs=slabs)
         finally:
             os.environ.pop("AM_FFT_CALLBACK", None)
             os.environ.pop("AM_NO_GRAPHS", None)

@@ -90,10 +90,12 @@ def test_slabs_match_single_fields(mods):
         assert rel(st[0], st0[0]) < 1e-12
 
 
-@pytest.mark.parametrize("transport", ["p2p", "nccl"])
-def test_nccl_single_rank(mods, tmp_path, transport):
+@pytest.mark.parametrize("transport,cb", [("p2p", "0"), ("nccl", "0"), ("p2p", "1"), ("nccl", "1")])
+def test_nccl_single_rank(mods, tmp_path, transport, cb):
     """One slab per process (world 1 here): fused P2P transposes or
-    ncclAlltoAll, with ncclAllReduce reductions, vs the local single-slab solver."""
+    ncclAlltoAll, with ncclAllReduce reductions, vs the local single-slab
+    solver; cb = 1: the inverse x transform reads ehat'/N through the load
+    callback (AM_FFT_CALLBACK=1)."""
     gsm, H, cfg = mods
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -102,7 +104,7 @@ def test_nccl_single_rank(mods, tmp_path, transport):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "dist", "worker_gpu.py"),
            str(out), transport]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=dict(os.environ, AM_FFT_CALLBACK=cb))
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     got = json.load(open(out))
     hom = H.Homogenizer(H.toy_mmc_grid(16), cfg)
