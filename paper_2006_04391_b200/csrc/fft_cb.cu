@@ -42,6 +42,20 @@ __device__ double2 am_z2d_load(void* in, unsigned long long off, void* info, voi
     const double2 v = c->ehat[off];
     return make_double2(v.x * c->inv_n, v.y * c->inv_n);
 }
+struct AmPackCb { double2* const* base; unsigned nzh, ny, nxl, nyl; };
+__device__ __forceinline__ double2* am_pack_addr(const AmPackCb* p, unsigned o) {
+    const unsigned kz = o % p->nzh, t = o / p->nzh;
+    const unsigned ky = t % p->ny, cx = t / p->ny;
+    const unsigned c = cx / p->nxl, xl = cx - c * p->nxl;
+    const unsigned j = ky / p->nyl, kyl = ky - j * p->nyl;
+    return p->base[j] + ((unsigned long long)(xl * 6 + c) * p->nyl + kyl) * p->nzh + kz;
+}
+__device__ void am_pack_store(void* out, unsigned long long off, double2 v, void* info, void* sh) {
+    *am_pack_addr((const AmPackCb*)info, (unsigned)off) = v;
+}
+__device__ double2 am_unpack_load(void* in, unsigned long long off, void* info, void* sh) {
+    return *am_pack_addr((const AmPackCb*)info, (unsigned)off);
+}
 )";
 
 struct Nvrtc {
@@ -110,13 +124,13 @@ size_t g_next = 0;
 
 }  // namespace
 
-// cufft plan *p (created here; cufftMakePlanMany64 geometry) whose first
-// pass loads its complex input through the callback reading d_info (a
-// device AmZ2DCb).  Returns false, with *p = 0, if the callback cannot be
+// cufft plan *p (created here; cufftMakePlanMany64 geometry) with the
+// callback `symbol` of kSource (a cufftXtCallbackType) reading d_info
+// (its device argument struct).  Returns false, with *p = 0, if the callback cannot be
 // linked in this process.
 bool am_callback_plan(cufftHandle* p, int rank, long long* n, long long* inembed, long long istride, long long idist,
                       long long* onembed, long long ostride, long long odist, cufftType type, long long batch,
-                      cudaStream_t stream, void* d_info) {
+                      cudaStream_t stream, void* d_info, const char* symbol, int cb_type) {
     std::lock_guard<std::mutex> lk(g_mu);
     *p = 0;
     if (g_state == 0) g_cands = nvrtc_candidates();
@@ -133,8 +147,8 @@ bool am_callback_plan(cufftHandle* p, int rank, long long* n, long long* inembed
         size_t ws = 0;
         void* info = d_info;
         bool ok = cufftCreate(&h) == CUFFT_SUCCESS &&
-                  cufftXtSetJITCallback(h, "am_z2d_load", g_ir.data(), g_ir.size(), CUFFT_CB_LD_COMPLEX_DOUBLE,
-                                        &info) == CUFFT_SUCCESS &&
+                  cufftXtSetJITCallback(h, symbol, g_ir.data(), g_ir.size(), (cufftXtCallbackType)cb_type, &info) ==
+                      CUFFT_SUCCESS &&
                   cufftMakePlanMany64(h, rank, n, inembed, istride, idist, onembed, ostride, odist, type, batch,
                                       &ws) == CUFFT_SUCCESS &&
                   cufftSetStream(h, stream) == CUFFT_SUCCESS;

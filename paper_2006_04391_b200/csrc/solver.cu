@@ -611,6 +611,9 @@ struct Slab {
     double2** peerE = nullptr;
     cufftHandle x1i = 0;        // inverse x transform reading ehat' / N through the load callback
     void* d_cbinfo = nullptr;   // its AmZ2DCb
+    cufftHandle r2p = 0, c2u = 0;  // 2-D D2Z storing / Z2D loading through the transpose callbacks
+    void* d_packinfo = nullptr;    // their AmPackCb
+    double2** dbase = nullptr;     // its block bases (device, one per slab)
     std::vector<Phase> phases;
 };
 
@@ -630,6 +633,7 @@ struct am_solver {
     ncclComm_t comm = nullptr;  // nccl mode: this process holds one slab
     std::vector<am::Slab> slabs;  // slabs held by this process
     cufftHandle r3 = 0, c3 = 0;   // 3-D D2Z / Z2D (single slab)
+    bool zpack = false;           // sigma's transposes ride on the 2-D transforms' callbacks (fft_cb.h)
     bool zcb = false;             // the inverse transform reads ehat' / N through a load callback (fft_cb.cu):
                                   // c3 (one slab) or every slab's x1i
     void* d_cbinfo = nullptr;     // c3's AmZ2DCb
@@ -681,8 +685,9 @@ static void solver_free(am_solver* h) {
         }
         cudaFree(s.eps); cudaFree(s.eps_n); cudaFree(s.sigma);
         cudaFree(s.S); cudaFree(s.ehat); cudaFree(s.P); cudaFree(s.X); cudaFree(s.flags); cudaFree(s.subs);
-        cudaFree(s.peerS); cudaFree(s.peerE); cudaFree(s.d_cbinfo);
-        if (s.x1i) cufftDestroy(s.x1i);
+        cudaFree(s.peerS); cudaFree(s.peerE); cudaFree(s.d_cbinfo); cudaFree(s.d_packinfo); cudaFree(s.dbase);
+        for (cufftHandle p : {s.x1i, s.r2p, s.c2u})
+            if (p) cufftDestroy(p);
     }
     cudaFree(h->red); cudaFreeHost(h->hred);
     cudaFree(h->Cbuf); cudaFree(h->status); cudaFree(h->stats); cudaFreeHost(h->hstats); cudaFree(h->dsmall);
@@ -760,8 +765,13 @@ static int forward(am_solver* h, double* Slab::*field, double2* Slab::*dst) {
         AM_CUFFT(cufftExecD2Z(h->r3, s.*field, s.*dst));
         return AM_OK;
     }
+    const bool fused = h->zpack && dst == &Slab::S;  // the D2Z stores the packed blocks itself
     if (h->p2p) {
         for (auto& s : h->slabs) {
+            if (fused) {
+                AM_CUFFT(cufftExecD2Z(s.r2p, s.*field, s.P));
+                continue;
+            }
             AM_CUFFT(cufftExecD2Z(h->r2, s.*field, s.P));
             k_pack_peer<<<runs_grid(h, s), 256, 0, h->stream>>>(s.P, dst == &Slab::S ? s.peerS : s.peerE, s.rank,
                                                                 s.nxl, h->ny, h->nzh, s.nyl);
@@ -772,6 +782,10 @@ static int forward(am_solver* h, double* Slab::*field, double2* Slab::*dst) {
         return AM_OK;
     }
     for (auto& s : h->slabs) {
+        if (fused) {
+            AM_CUFFT(cufftExecD2Z(s.r2p, s.*field, s.P));
+            continue;
+        }
         AM_CUFFT(cufftExecD2Z(h->r2, s.*field, s.P));
         k_pack<<<runs_grid(h, s), 256, 0, h->stream>>>(s.P, s.X, s.nxl, h->ny, h->nzh, s.nyl);
         AM_CUDA(cudaGetLastError());
@@ -791,8 +805,14 @@ static int inverse(am_solver* h, double2* Slab::*src, double* Slab::*field) {
     // S: the load callback reads ehat' / N instead (the caller skipped the copy)
     for (auto& s : h->slabs)
         AM_CUFFT(cufftExecZ2Z(h->zcb && src == &Slab::S ? s.x1i : h->x1, s.*src, s.*src, CUFFT_INVERSE));
+    const bool fused = h->zpack && src == &Slab::S;  // the Z2D loads the blocks itself
     if (h->p2p) {
         AM_TRY(barrier(h));  // every rank's x-transform is done before it is read
+        if (fused) {
+            for (auto& s : h->slabs) AM_CUFFT(cufftExecZ2D(s.c2u, s.P, s.*field));
+            AM_TRY(barrier(h));  // nobody overwrites a spectrum a peer is still reading
+            return AM_OK;
+        }
         for (auto& s : h->slabs) {
             k_unpack_peer<<<runs_grid(h, s), 256, 0, h->stream>>>(src == &Slab::S ? s.peerS : s.peerE, s.P, s.rank,
                                                                   s.nxl, h->ny, h->nzh, s.nyl);
@@ -804,6 +824,10 @@ static int inverse(am_solver* h, double2* Slab::*src, double* Slab::*field) {
     }
     AM_TRY(alltoall(h, src, &Slab::X, (size_t)6 * h->slabs[0].nxl * h->slabs[0].nyl * h->nzh));
     for (auto& s : h->slabs) {
+        if (fused) {
+            AM_CUFFT(cufftExecZ2D(s.c2u, s.P, s.*field));
+            continue;
+        }
         k_unpack<<<runs_grid(h, s), 256, 0, h->stream>>>(s.X, s.P, s.nxl, h->ny, h->nzh, s.nyl);
         AM_CUDA(cudaGetLastError());
         AM_CUFFT(cufftExecZ2D(h->c2, s.P, s.*field));
@@ -1065,7 +1089,7 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
             h->zcb = cudaMalloc(&h->d_cbinfo, sizeof(info)) == cudaSuccess &&
                      cudaMemcpy(h->d_cbinfo, &info, sizeof(info), cudaMemcpyHostToDevice) == cudaSuccess &&
                      am_callback_plan(&h->c3, 3, n3, nullptr, 1, (long long)nx * ny * h->nzh, nullptr, 1, N, CUFFT_Z2D,
-                                      6, h->stream, h->d_cbinfo);
+                                      6, h->stream, h->d_cbinfo, "am_z2d_load", CUFFT_CB_LD_COMPLEX_DOUBLE);
         }
         if (ok && !h->zcb)
             ok = plan(&h->c3, 3, n3, nullptr, 1, (long long)nx * ny * h->nzh, nullptr, 1, N, CUFFT_Z2D, 6);
@@ -1093,9 +1117,41 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
                 const AmZ2DCb info{sl.ehat, 1.0 / (double)N};
                 all = all && cudaMalloc(&sl.d_cbinfo, sizeof(info)) == cudaSuccess &&
                       cudaMemcpy(sl.d_cbinfo, &info, sizeof(info), cudaMemcpyHostToDevice) == cudaSuccess &&
-                      am_callback_plan(&sl.x1i, 1, n1, n1, bx, 1, n1, bx, 1, CUFFT_Z2Z, bx, h->stream, sl.d_cbinfo);
+                      am_callback_plan(&sl.x1i, 1, n1, n1, bx, 1, n1, bx, 1, CUFFT_Z2Z, bx, h->stream, sl.d_cbinfo,
+                                       "am_z2d_load", CUFFT_CB_LD_COMPLEX_DOUBLE);
             }
             h->zcb = all;
+        }
+        // sigma's transposes on the 2-D transforms' callbacks (fft_cb.h):
+        // block bases = the sibling slabs' spectra (local), the all-to-all
+        // buffer (NCCL; am_solver_ipc_import switches them to the peers')
+        const long long blk = (long long)nxl * 6 * nyl * h->nzh;
+        const bool fits = 6.0 * nxl * ny * h->nzh < 4294967296.0;  // 32-bit element offsets in the callbacks
+        if (ok && fits && !h->xfused && (cbenv ? cbenv[0] == '1' : N >= (int64_t(1) << 21))) {
+            bool all = true;
+            std::vector<double2*> byrank(nslabs, nullptr);
+            for (auto& sl : h->slabs) byrank[sl.rank] = sl.S;
+            for (auto& sl : h->slabs) {
+                std::vector<double2*> base(nslabs);
+                for (int j = 0; j < nslabs; ++j) base[j] = comm ? sl.X + j * blk : byrank[j] + sl.rank * blk;
+                const AmPackCb info{nullptr, (unsigned)h->nzh, (unsigned)ny, (unsigned)nxl, (unsigned)nyl};
+                all = all && cudaMalloc(&sl.dbase, sizeof(double2*) * nslabs) == cudaSuccess &&
+                      cudaMemcpy(sl.dbase, base.data(), sizeof(double2*) * nslabs, cudaMemcpyHostToDevice) ==
+                          cudaSuccess &&
+                      cudaMalloc(&sl.d_packinfo, sizeof(info)) == cudaSuccess;
+                if (!all) break;
+                AmPackCb dinfo = info;
+                dinfo.base = sl.dbase;
+                all = cudaMemcpy(sl.d_packinfo, &dinfo, sizeof(dinfo), cudaMemcpyHostToDevice) == cudaSuccess &&
+                      am_callback_plan(&sl.r2p, 2, n2, nullptr, 1, (long long)ny * nz, nullptr, 1,
+                                       (long long)ny * h->nzh, CUFFT_D2Z, 6LL * nxl, h->stream, sl.d_packinfo,
+                                       "am_pack_store", CUFFT_CB_ST_COMPLEX_DOUBLE) &&
+                      am_callback_plan(&sl.c2u, 2, n2, nullptr, 1, (long long)ny * h->nzh, nullptr, 1,
+                                       (long long)ny * nz, CUFFT_Z2D, 6LL * nxl, h->stream, sl.d_packinfo,
+                                       "am_unpack_load", CUFFT_CB_LD_COMPLEX_DOUBLE);
+                if (!all) break;
+            }
+            h->zpack = all;
         }
     }
     if (!ok) return bail(fail(AM_ERR_CUDA, "cufft plan creation failed for %dx%dx%d / %d slabs", nx, ny, nz, nslabs));
@@ -1186,6 +1242,12 @@ extern "C" int am_solver_ipc_import(am_solver* h, const void* all, int nranks) {
     }
     AM_CUDA(cudaMemcpy(sl.peerS, S.data(), sizeof(double2*) * nranks, cudaMemcpyHostToDevice));
     AM_CUDA(cudaMemcpy(sl.peerE, E.data(), sizeof(double2*) * nranks, cudaMemcpyHostToDevice));
+    if (h->zpack) {  // the transpose callbacks now address the peers' spectra (this rank's block)
+        const long long blk = (long long)sl.nxl * 6 * sl.nyl * h->nzh;
+        std::vector<double2*> base(nranks);
+        for (int r = 0; r < nranks; ++r) base[r] = S[r] + sl.rank * blk;
+        AM_CUDA(cudaMemcpy(sl.dbase, base.data(), sizeof(double2*) * nranks, cudaMemcpyHostToDevice));
+    }
     AM_CUDA(cudaMemsetAsync(h->dsmall, 0, sizeof(double) * 64, h->stream));
     AM_CUDA(cudaStreamSynchronize(h->stream));
     h->p2p = true;
@@ -1434,7 +1496,7 @@ extern "C" int am_solver_set_warm_start(am_solver* h, int on) {
 
 extern "C" int am_solver_fft_callback(const am_solver* h, int* on) {
     if (!h || !on) return fail(AM_ERR_ARG, "null argument");
-    *on = h->zcb ? 1 : 0;
+    *on = (h->zcb ? 1 : 0) | (h->zpack ? 2 : 0);
     return AM_OK;
 }
 
