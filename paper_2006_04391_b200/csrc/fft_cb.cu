@@ -126,11 +126,12 @@ size_t g_next = 0;
 
 // cufft plan *p (created here; cufftMakePlanMany64 geometry) with the
 // callback `symbol` of kSource (a cufftXtCallbackType) reading d_info
-// (its device argument struct).  Returns false, with *p = 0, if the callback cannot be
+// (its device argument struct).  ws_max != nullptr: no work area of its
+// own; *ws_max is raised to the plan's need (the caller sets a shared one).  Returns false, with *p = 0, if the callback cannot be
 // linked in this process.
 bool am_callback_plan(cufftHandle* p, int rank, long long* n, long long* inembed, long long istride, long long idist,
                       long long* onembed, long long ostride, long long odist, cufftType type, long long batch,
-                      cudaStream_t stream, void* d_info, const char* symbol, int cb_type) {
+                      cudaStream_t stream, void* d_info, const char* symbol, int cb_type, size_t* ws_max) {
     std::lock_guard<std::mutex> lk(g_mu);
     *p = 0;
     if (g_state == 0) g_cands = nvrtc_candidates();
@@ -147,6 +148,7 @@ bool am_callback_plan(cufftHandle* p, int rank, long long* n, long long* inembed
         size_t ws = 0;
         void* info = d_info;
         bool ok = cufftCreate(&h) == CUFFT_SUCCESS &&
+                  (!ws_max || cufftSetAutoAllocation(h, 0) == CUFFT_SUCCESS) &&
                   cufftXtSetJITCallback(h, symbol, g_ir.data(), g_ir.size(), (cufftXtCallbackType)cb_type, &info) ==
                       CUFFT_SUCCESS &&
                   cufftMakePlanMany64(h, rank, n, inembed, istride, idist, onembed, ostride, odist, type, batch,
@@ -154,6 +156,7 @@ bool am_callback_plan(cufftHandle* p, int rank, long long* n, long long* inembed
                   cufftSetStream(h, stream) == CUFFT_SUCCESS;
         if (ok) {
             *p = h;
+            if (ws_max && ws > *ws_max) *ws_max = ws;
             return true;
         }
         if (h) cufftDestroy(h);

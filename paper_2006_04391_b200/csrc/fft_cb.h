@@ -22,4 +22,4 @@ struct AmPackCb {
 
 bool am_callback_plan(cufftHandle* p, int rank, long long* n, long long* inembed, long long istride, long long idist,
                       long long* onembed, long long ostride, long long odist, cufftType type, long long batch,
-                      cudaStream_t stream, void* d_info, const char* symbol, int cb_type);
+                      cudaStream_t stream, void* d_info, const char* symbol, int cb_type, size_t* ws_max);

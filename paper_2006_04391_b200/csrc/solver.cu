@@ -634,6 +634,7 @@ struct am_solver {
     std::vector<am::Slab> slabs;  // slabs held by this process
     cufftHandle r3 = 0, c3 = 0;   // 3-D D2Z / Z2D (single slab)
     bool zpack = false;           // sigma's transposes ride on the 2-D transforms' callbacks (fft_cb.h)
+    void* fftws = nullptr;        // the cufft plans' shared work area
     bool zcb = false;             // the inverse transform reads ehat' / N through a load callback (fft_cb.cu):
                                   // c3 (one slab) or every slab's x1i
     void* d_cbinfo = nullptr;     // c3's AmZ2DCb
@@ -692,7 +693,7 @@ static void solver_free(am_solver* h) {
     cudaFree(h->red); cudaFreeHost(h->hred);
     cudaFree(h->Cbuf); cudaFree(h->status); cudaFree(h->stats); cudaFreeHost(h->hstats); cudaFree(h->dsmall);
     cudaFree(h->pl); cudaFreeHost(h->hpl); cudaFree(h->ps); cudaFreeHost(h->hps);
-    cudaFree(h->d_eb); cudaFreeHost(h->h_eb); cudaFree(h->d_cbinfo);
+    cudaFree(h->d_eb); cudaFreeHost(h->h_eb); cudaFree(h->d_cbinfo); cudaFree(h->fftws);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     for (cufftHandle p : {h->r3, h->c3, h->r2, h->c2, h->x1})
@@ -1065,13 +1066,18 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
     AMC(cudaMalloc(&h->ps, sizeof(double) * kStat * h->nstat));
     AMC(cudaMallocHost(&h->hps, sizeof(double) * kStat * h->nstat));
 #undef AMC
-    size_t ws = 0;
+    // every plan runs on h->stream, one at a time: they share one work area
+    // (640^3: the 3-D D2Z and Z2D each want 12.6 GB)
+    size_t ws_max = 0;
     auto plan = [&](cufftHandle* p, int rank, long long* n, long long* inembed, long long istride, long long idist,
                     long long* onembed, long long ostride, long long odist, cufftType t, long long batch) -> bool {
-        return cufftCreate(p) == CUFFT_SUCCESS &&
-               cufftMakePlanMany64(*p, rank, n, inembed, istride, idist, onembed, ostride, odist, t, batch, &ws) ==
-                   CUFFT_SUCCESS &&
-               cufftSetStream(*p, h->stream) == CUFFT_SUCCESS;
+        size_t ws = 0;
+        const bool r = cufftCreate(p) == CUFFT_SUCCESS && cufftSetAutoAllocation(*p, 0) == CUFFT_SUCCESS &&
+                       cufftMakePlanMany64(*p, rank, n, inembed, istride, idist, onembed, ostride, odist, t, batch,
+                                           &ws) == CUFFT_SUCCESS &&
+                       cufftSetStream(*p, h->stream) == CUFFT_SUCCESS;
+        ws_max = std::max(ws_max, ws);
+        return r;
     };
     bool ok;
     // the inverse transform with the load callback (fft_cb.cu) from 128^3
@@ -1089,7 +1095,7 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
             h->zcb = cudaMalloc(&h->d_cbinfo, sizeof(info)) == cudaSuccess &&
                      cudaMemcpy(h->d_cbinfo, &info, sizeof(info), cudaMemcpyHostToDevice) == cudaSuccess &&
                      am_callback_plan(&h->c3, 3, n3, nullptr, 1, (long long)nx * ny * h->nzh, nullptr, 1, N, CUFFT_Z2D,
-                                      6, h->stream, h->d_cbinfo, "am_z2d_load", CUFFT_CB_LD_COMPLEX_DOUBLE);
+                                      6, h->stream, h->d_cbinfo, "am_z2d_load", CUFFT_CB_LD_COMPLEX_DOUBLE, &ws_max);
         }
         if (ok && !h->zcb)
             ok = plan(&h->c3, 3, n3, nullptr, 1, (long long)nx * ny * h->nzh, nullptr, 1, N, CUFFT_Z2D, 6);
@@ -1118,7 +1124,7 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
                 all = all && cudaMalloc(&sl.d_cbinfo, sizeof(info)) == cudaSuccess &&
                       cudaMemcpy(sl.d_cbinfo, &info, sizeof(info), cudaMemcpyHostToDevice) == cudaSuccess &&
                       am_callback_plan(&sl.x1i, 1, n1, n1, bx, 1, n1, bx, 1, CUFFT_Z2Z, bx, h->stream, sl.d_cbinfo,
-                                       "am_z2d_load", CUFFT_CB_LD_COMPLEX_DOUBLE);
+                                       "am_z2d_load", CUFFT_CB_LD_COMPLEX_DOUBLE, &ws_max);
             }
             h->zcb = all;
         }
@@ -1145,16 +1151,24 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
                 all = cudaMemcpy(sl.d_packinfo, &dinfo, sizeof(dinfo), cudaMemcpyHostToDevice) == cudaSuccess &&
                       am_callback_plan(&sl.r2p, 2, n2, nullptr, 1, (long long)ny * nz, nullptr, 1,
                                        (long long)ny * h->nzh, CUFFT_D2Z, 6LL * nxl, h->stream, sl.d_packinfo,
-                                       "am_pack_store", CUFFT_CB_ST_COMPLEX_DOUBLE) &&
+                                       "am_pack_store", CUFFT_CB_ST_COMPLEX_DOUBLE, &ws_max) &&
                       am_callback_plan(&sl.c2u, 2, n2, nullptr, 1, (long long)ny * h->nzh, nullptr, 1,
                                        (long long)ny * nz, CUFFT_Z2D, 6LL * nxl, h->stream, sl.d_packinfo,
-                                       "am_unpack_load", CUFFT_CB_LD_COMPLEX_DOUBLE);
+                                       "am_unpack_load", CUFFT_CB_LD_COMPLEX_DOUBLE, &ws_max);
                 if (!all) break;
             }
             h->zpack = all;
         }
     }
     if (!ok) return bail(fail(AM_ERR_CUDA, "cufft plan creation failed for %dx%dx%d / %d slabs", nx, ny, nz, nslabs));
+    if (ws_max) {
+        if (cudaMalloc(&h->fftws, ws_max) != cudaSuccess) return bail(fail(AM_ERR_CUDA, "out of memory (cufft work area)"));
+        std::vector<cufftHandle> all = {h->r3, h->c3, h->r2, h->c2, h->x1};
+        for (auto& sl : h->slabs) all.insert(all.end(), {sl.x1i, sl.r2p, sl.c2u});
+        for (cufftHandle p : all)
+            if (p && cufftSetWorkArea(p, h->fftws) != CUFFT_SUCCESS)
+                return bail(fail(AM_ERR_CUDA, "cufft work area"));
+    }
     if (h->multi) {
         for (auto& sl : h->slabs) {
             if (cudaMalloc(&sl.peerS, sizeof(double2*) * nslabs) != cudaSuccess ||
