@@ -1085,6 +1085,12 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
     // origin's N ebar / N is then exact); AM_FFT_CALLBACK=0 / 1 forces it
     // off / on.  The callback's first link in a process costs ~2 s.
     const char* cbenv = getenv("AM_FFT_CALLBACK");
+    // local slabs transpose through the siblings' spectra (the P2P kernels);
+    // AM_LOCAL_ALLTOALL=1 runs them through the all-to-all buffers instead
+    // (device copies in place of ncclAlltoAll: the NCCL transport's data
+    // layout with more than one slab, testable on one GPU)
+    const char* ltenv = getenv("AM_LOCAL_ALLTOALL");
+    const bool local_p2p = !comm && !(ltenv && ltenv[0] == '1');
     const bool want_cb = !h->xfused && (N & (N - 1)) == 0 && (cbenv ? cbenv[0] == '1' : N >= (int64_t(1) << 21));
     if (!h->multi) {
         long long n3[3] = {nx, ny, nz};
@@ -1139,7 +1145,7 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
             for (auto& sl : h->slabs) byrank[sl.rank] = sl.S;
             for (auto& sl : h->slabs) {
                 std::vector<double2*> base(nslabs);
-                for (int j = 0; j < nslabs; ++j) base[j] = comm ? sl.X + j * blk : byrank[j] + sl.rank * blk;
+                for (int j = 0; j < nslabs; ++j) base[j] = local_p2p ? byrank[j] + sl.rank * blk : sl.X + j * blk;
                 const AmPackCb info{nullptr, (unsigned)h->nzh, (unsigned)ny, (unsigned)nxl, (unsigned)nyl};
                 all = all && cudaMalloc(&sl.dbase, sizeof(double2*) * nslabs) == cudaSuccess &&
                       cudaMemcpy(sl.dbase, base.data(), sizeof(double2*) * nslabs, cudaMemcpyHostToDevice) ==
@@ -1185,7 +1191,7 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
                 if (cudaMemcpy(sl.peerS, S.data(), sizeof(double2*) * nslabs, cudaMemcpyHostToDevice) != cudaSuccess ||
                     cudaMemcpy(sl.peerE, E.data(), sizeof(double2*) * nslabs, cudaMemcpyHostToDevice) != cudaSuccess)
                     return bail(fail(AM_ERR_CUDA, "copy failed"));
-            h->p2p = true;
+            h->p2p = local_p2p;
         }
     }
     *out = h;

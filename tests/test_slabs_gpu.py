@@ -134,3 +134,36 @@ def test_slab_count_independent_bits(mods, parity_log):
     same = {k: recs[k] == recs[2] for k in (4, 8)}
     parity_log("slab_bits", **{f"slabs{k}_equal_to_2": v for k, v in same.items()})
     assert all(same.values()), recs
+
+
+@pytest.mark.parametrize("cb", ["0", "1"])
+@pytest.mark.parametrize("slabs", [2, 4])
+def test_local_alltoall_transport_bitwise(mods, slabs, cb):
+    """The NCCL transport's data layout with more than one slab, on one GPU:
+    AM_LOCAL_ALLTOALL=1 sends the local slabs' transposes through the
+    all-to-all buffers (device copies in place of ncclAlltoAll; with
+    AM_FFT_CALLBACK=1 the 2-D transforms' callbacks write / read those
+    buffers).  Fields and histories are bitwise those of the sibling-P2P
+    transposes (pure data movement)."""
+    gsm, H, cfg = mods
+    out = []
+    for lt in ("0", "1"):
+        os.environ["AM_LOCAL_ALLTOALL"] = lt
+        os.environ["AM_FFT_CALLBACK"] = cb
+        try:
+            hom = H.Homogenizer(H.toy_mmc_grid(16), cfg, slabs=slabs)
+        finally:
+            os.environ.pop("AM_LOCAL_ALLTOALL", None)
+            os.environ.pop("AM_FFT_CALLBACK", None)
+        path = H.LoadingPath(steps=20)
+        t = path.times()
+        res = []
+        for k in (1, 2):
+            eb = np.zeros(6)
+            eb[0] = path.eps_xx(t[k])
+            eps, sig, info = hom.solve_step(eb, t[k] - t[k - 1], free_mask=np.array([False] + [True] * 5))
+            res.append((eps, sig, info.history))
+            hom.commit_step(eps, eps.mean(axis=(1, 2, 3)))
+        out.append(res)
+    for (e0, s0, h0), (e1, s1, h1) in zip(*out):
+        assert np.array_equal(e0, e1) and np.array_equal(s0, s1) and h0 == h1
