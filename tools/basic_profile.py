@@ -1,6 +1,6 @@
 """A few basic-scheme iterations at n^3 for ncu (launch list / full capture).
 
-usage: python tools/basic_profile.py [n] [iterations] [warm]
+usage: python tools/basic_profile.py [n] [iterations] [warm|cold] [slabs]
 """
 import os
 import sys
@@ -14,8 +14,9 @@ from paper_2006_04391_b200.evaluator import StrategyConfig  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 its = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 warm = len(sys.argv) > 3 and sys.argv[3] == "warm"
+slabs = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 hom = H.Homogenizer(H.toy_mmc_grid(n), StrategyConfig(strategy="automatic", integrator="implicit-euler"),
-                    max_iterations=its, newton_warm_start=warm)
+                    max_iterations=its, newton_warm_start=warm, slabs=slabs)
 path = H.LoadingPath(steps=20)
 t = path.times()
 eb = np.zeros(6)
