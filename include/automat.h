@@ -248,8 +248,8 @@ int am_solver_set_warm_start(am_solver *h, int on);
  * spectrum through a cuFFT load callback (the 3-D inverse on one slab, every
  * slab's inverse x transform on x slabs; power-of-two voxel counts), 2 if
  * sigma's slab transposes ride on the 2-D transforms' store / load callbacks
- * (x slabs).  Both from 128^3 on, or AM_FFT_CALLBACK=1; fields bitwise those
- * of the copy / pack-kernel paths.  No
+ * (x slabs).  Both for power-of-two voxel counts from 128^3 on, or
+ * AM_FFT_CALLBACK=1; fields bitwise those of the copy / pack-kernel paths.  No
  * reference counterpart (implementation detail of homogenize.py:458-460). */
 int am_solver_fft_callback(const am_solver *h, int *on);
 /* Homogenizer.commit_step (homogenize.py:474-480) for the solver's eps:

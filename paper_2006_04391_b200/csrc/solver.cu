@@ -1139,7 +1139,9 @@ static int solver_build(int nx, int ny, int nz, const uint8_t* ids, int nmat, co
         // buffer (NCCL; am_solver_ipc_import switches them to the peers')
         const long long blk = (long long)nxl * 6 * nyl * h->nzh;
         const bool fits = 6.0 * nxl * ny * h->nzh < 4294967296.0;  // 32-bit element offsets in the callbacks
-        if (ok && fits && !h->xfused && (cbenv ? cbenv[0] == '1' : N >= (int64_t(1) << 21))) {
+        // (power-of-two grids, like the load callback: cuFFT picks other kernels
+        // for LTO plans of other sizes, and the fields would differ in the last bits)
+        if (ok && fits && (N & (N - 1)) == 0 && !h->xfused && (cbenv ? cbenv[0] == '1' : N >= (int64_t(1) << 21))) {
             bool all = true;
             std::vector<double2*> byrank(nslabs, nullptr);
             for (auto& sl : h->slabs) byrank[sl.rank] = sl.S;
