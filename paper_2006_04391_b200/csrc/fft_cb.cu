@@ -127,8 +127,10 @@ size_t g_next = 0;
 // cufft plan *p (created here; cufftMakePlanMany64 geometry) with the
 // callback `symbol` of kSource (a cufftXtCallbackType) reading d_info
 // (its device argument struct).  ws_max != nullptr: no work area of its
-// own; *ws_max is raised to the plan's need (the caller sets a shared one).  Returns false, with *p = 0, if the callback cannot be
-// linked in this process.
+// own; *ws_max is raised to the plan's need (the caller sets a shared
+// one).  Returns false, with *p = 0, if the callback cannot be linked in
+// this process; a failed link moves on to the next NVRTC candidate, and
+// once none is left the process stays on the copy / pack-kernel paths.
 bool am_callback_plan(cufftHandle* p, int rank, long long* n, long long* inembed, long long istride, long long idist,
                       long long* onembed, long long ostride, long long odist, cufftType type, long long batch,
                       cudaStream_t stream, void* d_info, const char* symbol, int cb_type, size_t* ws_max) {
