@@ -167,3 +167,35 @@ def test_local_alltoall_transport_bitwise(mods, slabs, cb):
         out.append(res)
     for (e0, s0, h0), (e1, s1, h1) in zip(*out):
         assert np.array_equal(e0, e1) and np.array_equal(s0, s1) and h0 == h1
+
+
+def test_callbacks_bitwise_at_256(mods):
+    """Config-4 grid on 8 slabs, the first 6 iterations of load step 1 with
+    the cuFFT callbacks (default at 256^3: inverse x transform loading
+    ehat'/N, sigma's transposes inside the 2-D transforms) and without
+    (AM_FFT_CALLBACK=0: scaled copy, pack / unpack kernels): residual
+    histories, strain and stress fields bitwise equal."""
+    import ctypes
+
+    gsm, H, cfg = mods
+    grid = H.toy_mmc_grid(256)
+    path = H.LoadingPath(steps=20)
+    t = path.times()
+    eb = np.zeros(6)
+    eb[0] = path.eps_xx(t[1])
+    out = []
+    for cb in ("0", "1"):
+        os.environ["AM_FFT_CALLBACK"] = cb
+        try:
+            hom = H.Homogenizer(grid, cfg, slabs=8, max_iterations=6)
+        finally:
+            os.environ.pop("AM_FFT_CALLBACK", None)
+        on = ctypes.c_int(-1)
+        hom._lib.am_solver_fft_callback(hom._h, ctypes.byref(on))
+        assert on.value == (3 if cb == "1" else 0)
+        with pytest.raises(H.SolverError) as exc:
+            hom._solve(eb, t[1] - t[0], np.array([False] + [True] * 5))
+        out.append((exc.value.history, hom._get(0), hom._get(2)))
+        del hom
+    (h0, e0, s0), (h1, e1, s1) = out
+    assert h0 == h1 and np.array_equal(e0, e1) and np.array_equal(s0, s1)
