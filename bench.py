@@ -789,13 +789,16 @@ def main():
             ph = np.zeros(5)
             _lib.check(hom._lib.am_solver_timing(hom._h, -1, _lib.ptr(ph)))
             k = ph[4] or 1.0
+            cbits = ctypes.c_int(0)
+            _lib.check(hom._lib.am_solver_fft_callback(hom._h, ctypes.byref(cbits)))
             return {"value": info.iterations / (ms * 1e-3), "unit": "it/s", "iterations": info.iterations,
                     "ms_per_iteration": ms / info.iterations,
+                    "fft_load_callback": bool(cbits.value & 1), "transposes_in_fft_callbacks": bool(cbits.value & 2),
                     "phase_ms_per_iteration": {"material": ph[0] / k, "forward_fft+transpose": ph[1] / k,
                                                "fourier+reduce": ph[2] / k,
                                                "origin+inverse_fft+transpose": ph[3] / max(k - 1, 1)},
-                    "config": {"workload": f"config 4 grid, load step 1, 8 x-slabs of one GPU (am_solver_create_slabs: "
-                                           "the multi-GPU algorithm with device-copy transposes)"}}
+                    "config": {"workload": "config 4 grid, load step 1, 8 x-slabs of one GPU (am_solver_create_slabs: "
+                                           "the multi-GPU algorithm, transposes through the sibling slabs' spectra)"}}
 
         guarded("config4_step1_slab_algorithm", slab_alg)
 
